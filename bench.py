@@ -1,0 +1,371 @@
+"""Benchmark of the Jacobi stencil sweep on B200 (driver contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+                    [--impl ours|reference] [--fused k] [--mode exact|fast]
+
+Default workload (N=1): BASELINE config C3, the north star's headline target —
+Heat-3D 7-point star fp64, 512^3 interior, halo 1, fill_random(seed=1), 1000
+time steps.  A "step" is one time step over the whole grid.  For N>1 every
+rank owns a 512^3 slab of a (512*N) x 512 x 512 grid (weak scaling, C5's
+slab + deep-halo scheme at C3's per-GPU size) and exchanges r*k-deep halos
+with its neighbours over NCCL once per k fused steps.
+
+`value` is device-resident throughput (GStencil/s = points * K / time, the
+reference's Eq. 6, proj/src/metrics.cpp:8-20), timed with CUDA events on the
+stream the sweeps launch on, max over ranks.  `e2e` is the same metric through
+the reference-facing call (naive_run on host buffers in pinned memory: H2D of
+the read buffer + K steps + D2H of both buffers' interiors).
+`--impl reference` times the reference's own CPU path (oracle/_ref: the
+unmodified reference sources, run_tessellated with all host threads).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(bench="Heat-2D", extent=[4096, 4096], dtype="f64", steps=100, fused=8,
+               mode="exact", workload="C1: 2D heat 5-point star fp64, 4096x4096, 100 timesteps",
+               ref_tile=[200, 200], ref_tb=50),
+    "c2": dict(bench="Box-2D9P", extent=[16384, 16384], dtype="f64", steps=100, fused=4,
+               mode="exact",
+               workload="C2: 2D 9-point box fp64, 16384x16384, temporal blocking k=4",
+               ref_tile=[2000, 2000], ref_tb=4),
+    "c3": dict(bench="Heat-3D", extent=[512, 512, 512], dtype="f64", steps=1000, fused=0,
+               mode="exact",
+               workload="C3: 3D heat 7-point star fp64, 512^3 per GPU, 1000 timesteps",
+               ref_tile=[20, 20, 20], ref_tb=10),
+    "c4": dict(bench="Box-3D27P", extent=[1024, 1024, 1024], dtype="f32", steps=100, fused=0,
+               mode="fast", workload="C4: 3D 27-point box fp32, 1024^3, fast (FMA) mode",
+               ref_tile=None, ref_tb=None),
+    "c5": dict(bench="Heat-3D", extent=[1024, 1024, 1024], dtype="f64", steps=100, fused=0,
+               mode="exact", workload="C5: 3D heat 7-point fp64, 1024^3 per GPU (weak scaling)",
+               ref_tile=[20, 20, 20], ref_tb=10),
+}
+
+HBM_FALLBACK_GBPS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBPS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "100"], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_grid(ts, cfg, extent, pinned=False, seed=1):
+    cls = ts.Grid if cfg["dtype"] == "f64" else ts.GridF
+    g = cls(extent, [1] * len(extent), pinned=pinned)
+    ts.fill_random(g, seed)
+    return g
+
+
+def fused_groups(steps: int, k: int) -> list[int]:
+    out = []
+    while steps > 0:
+        out.append(min(k, steps))
+        steps -= out[-1]
+    return out
+
+
+def ncu_traffic(cfg_name: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(cfg_name)
+    except Exception:
+        return None
+
+
+def cpu_baseline(ts, cfg, cfg_name, steps_cap=None):
+    """The reference's own CPU path on this host (oracle/_ref), bounded sample."""
+    import oracle
+    if not oracle.Reference.available():
+        return None
+    ref = oracle.Reference()
+    threads = os.cpu_count() or 1
+    k = ts.find_benchmark(cfg["bench"]).kernel
+    if cfg["dtype"] == "f64":
+        extent = cfg["extent"]
+        g = make_grid(ts, cfg, extent)
+        steps = cfg["ref_tb"] * (1 if steps_cap is None else max(1, steps_cap // cfg["ref_tb"]))
+        (upd, rounds, trailing), sec = ref.run_tessellated(g, k, steps, cfg["ref_tile"],
+                                                           cfg["ref_tb"], threads)
+        value = upd / sec / 1e9
+        return {"value": round(value, 4), "unit": "GStencil/s", "cores": threads,
+                "kind": "reference",
+                "sample": (f"reference run_tessellated(tile={cfg['ref_tile']}, "
+                           f"tb={cfg['ref_tb']}, threads={threads}) on the full "
+                           f"{'x'.join(map(str, extent))} grid, T={steps}")}
+    # fp32: the reference has no threaded fp32 path; naive_run<float>, 1 thread,
+    # on a slab of the full cross-section.
+    extent = [64] + cfg["extent"][1:]
+    g = make_grid(ts, cfg, extent)
+    sec = ref.time_naive_f32(g, k, 1)
+    pts = 1
+    for e in extent:
+        pts *= e
+    return {"value": round(pts / sec / 1e9, 4), "unit": "GStencil/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"reference naive_run<float> 1 thread on a {'x'.join(map(str, extent))} "
+                      f"slab, T=1"}
+
+
+def run_reference_arm(args, cfg, cfg_name):
+    import paper_2303_08365_b200 as ts
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    t_steps = min(args.steps, 20)
+    cb = cpu_baseline(ts, cfg, cfg_name, steps_cap=t_steps)
+    if cb is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libtessera_ref.so not built (make -C oracle ref)"}))
+        return
+    line = {"metric": "GStencil/s (fp64) at 1/2/4/8 B200 and % of HBM roofline vs host-CPU ref",
+            "impl": "reference", "value": cb["value"], "unit": "GStencil/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if cfg["dtype"] == "f64" else "f32",
+            "data": "synthetic: fill_random(seed=1) U[0,1) interior, zero Dirichlet halo",
+            "config": {"workload": cfg["workload"], "extent": cfg["extent"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "GStencil/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--fused", type=int, default=None)
+    ap.add_argument("--mode", default=None, choices=["exact", "fast"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    args.steps = cfg["steps"] if args.steps is None else args.steps
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg, args.config)
+
+    import torch
+    import paper_2303_08365_b200 as ts
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    mode = args.mode or cfg["mode"]
+    fused_req = cfg["fused"] if args.fused is None else args.fused
+    k = ts.find_benchmark(cfg["bench"]).kernel
+    esize = 8 if cfg["dtype"] == "f64" else 4
+    per_gpu = list(cfg["extent"])
+    points_per_gpu = 1
+    for e in per_gpu:
+        points_per_gpu *= e
+    stream = torch.cuda.current_stream(dev)
+
+    if world == 1:
+        host = make_grid(ts, cfg, per_gpu)
+        state = ts.DeviceGrid(host, dev)
+        # resolve the engine's fused step count
+        probe = state.advance(k, 1, fused_steps=fused_req, mode=mode)
+        kfused = probe.fused_steps
+        engine = probe.engine
+        advance = lambda n: state.advance(k, n, fused_steps=kfused, mode=mode)  # noqa: E731
+        comm = None
+    else:
+        from paper_2303_08365_b200.partition import SlabRunner, plan_slabs
+        kfused_guess = fused_req if fused_req else 1
+        glob = [per_gpu[0] * world] + per_gpu[1:]
+        plan = plan_slabs(glob, k.radius, kfused_guess, world, rank)
+        runner = SlabRunner.synthetic(ts, k, plan, cfg["dtype"], dev, seed=1 + rank,
+                                      fused_steps=kfused_guess, mode=mode)
+        kfused = runner.fused_steps
+        engine = 2
+        advance = runner.advance
+        comm = runner
+
+    groups = fused_groups(args.steps, kfused)
+    for n in fused_groups(args.warmup, kfused):
+        advance(n)
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(groups) + 1)]
+    launches = 0
+    ev[0].record(stream)
+    for i, n in enumerate(groups):
+        st = advance(n)
+        launches += st.kernel_launches
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    elapsed_ms = ev[0].elapsed_time(ev[-1])
+    full = [ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(groups) if n == kfused]
+    launch_ms = statistics.mean(full) if full else elapsed_ms / max(1, len(groups))
+    if dist:
+        t = torch.tensor([elapsed_ms, launch_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, launch_ms = float(t[0]), float(t[1])
+        lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+        dist.all_reduce(lt)
+        launches = int(lt[0])
+
+    total_points = points_per_gpu * world
+    value = total_points * args.steps / (elapsed_ms / 1e3) / 1e9
+    peak, peak_kind = peaks()
+    # Algorithmic bytes of one fused launch on one GPU: 2*sizeof(T) per stencil
+    # update (one compulsory read + one write per step), times
+    # the k steps the launch advances ("HBM-equivalent" for k > 1).
+    alg_bytes = 2 * esize * points_per_gpu * kfused
+    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+    traffic = ncu_traffic(args.config)
+
+    e2e = None
+    cpu = None
+    if rank == 0 and world == 1:
+        if not args.no_e2e:
+            hg = make_grid(ts, cfg, per_gpu, pinned=True)
+            ts.run_gpu(hg, k, min(4, args.steps), fused_steps=kfused, mode=mode)  # warm
+            ts.fill_random(hg, 1)
+            t0 = time.perf_counter()
+            st = ts.run_gpu(hg, k, args.steps, fused_steps=kfused, mode=mode)
+            wall = time.perf_counter() - t0
+            e2e = {"value": round(total_points * args.steps / wall / 1e9, 3),
+                   "unit": "GStencil/s",
+                   "h2d_bytes_per_step": round(st.h2d_bytes / args.steps, 1),
+                   "d2h_bytes_per_step": round(st.d2h_bytes / args.steps, 1),
+                   "call": "paper_2303_08365_b200.run_gpu(pinned Grid) -> tsr_run",
+                   "wall_s": round(wall, 4)}
+            del hg
+        if not args.no_cpu:
+            cpu = cpu_baseline(ts, cfg, args.config)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": "GStencil/s (fp64) at 1/2/4/8 B200 and % of HBM roofline vs host-CPU ref",
+        "value": round(value, 3),
+        "unit": "GStencil/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(elapsed_ms / args.steps, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": cfg["dtype"],
+        "data": "synthetic: fill_random(seed=1) U[0,1) interior, zero Dirichlet halo",
+        "config": {"workload": cfg["workload"], "extent_per_gpu": per_gpu,
+                   "global_extent": [per_gpu[0] * world] + per_gpu[1:],
+                   "kernel": cfg["bench"], "mode": mode, "fused_steps": kfused,
+                   "engine": {1: "generic", 2: "tuned"}.get(engine, str(engine)),
+                   "parallelism": f"slab{world}" if world > 1 else "single",
+                   "l2": (f"no flush: the two buffers ({2 * esize * points_per_gpu / 1e9:.2f} GB)"
+                          " exceed the 126 MB L2")},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic,
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
+                     if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
+                     "basis": (f"algorithmic {2 * esize} B per stencil update x {kfused} fused "
+                               f"steps per launch / mean CUDA-event launch time "
+                               f"{launch_ms:.4f} ms")},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if comm is not None:
+        line["comm"] = comm.comm_summary()
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,211 @@
+"""CPU oracle for the Jacobi stencil sweep — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` /
+``--impl reference`` legs may import this package, and only as the checker or
+as the timed CPU baseline; the product (paper_2303_08365_b200/) never does.
+
+Two checkers live here:
+
+* ``Oracle`` wraps ``liboracle.so``, the C restatement in oracle.c of the
+  reference's apply_box / naive_run / fill_random / max_rel_deviation
+  (file:line citations in oracle.c).  Parity is PINNED: tests/test_oracle.py
+  checks it bitwise against the reference library and the golden fixtures.
+* ``Reference`` wraps ``_ref/libtessera_ref.so``: the UNMODIFIED reference
+  sources under /root/reference/proj/src compiled by oracle/Makefile (plus the
+  extern "C" shim ref_shim.cpp).  It exists wherever the build ran here (it
+  travels to the GPU box inside the repo snapshot).
+
+Both operate in place on grids of the product's host Grid type, whose layout
+is the reference's own (proj/include/tessera/grid.hpp:46-49).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libtessera_ref.so")
+REF_ROOT = "/root/reference/proj"
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_f64p = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+def build(ref: bool = True) -> None:
+    """Builds liboracle.so and (when /root/reference exists) _ref/."""
+    subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
+    if ref and os.path.isdir(REF_ROOT):
+        subprocess.run(["make", "-s", "-j8", "-C", HERE, "ref"], check=True)
+
+
+def _geom(grid):
+    ext = (ctypes.c_int64 * 3)(*(grid.extent + [1] * (3 - grid.dims)))
+    halo = (ctypes.c_int64 * 3)(*(grid.halo + [0] * (3 - grid.dims)))
+    return ext, halo
+
+
+def _taps(kernel):
+    taps = kernel.tap_list()
+    offs = (ctypes.c_int32 * (3 * len(taps)))(*[v for o, _ in taps for v in o])
+    ws = (ctypes.c_double * len(taps))(*[w for _, w in taps])
+    return len(taps), offs, ws
+
+
+def _sfx(grid) -> str:
+    return "f64" if grid.dtype == np.float64 else "f32"
+
+
+class Oracle:
+    """The C restatement (oracle.c)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build(ref=False)
+        self.L = ctypes.CDLL(path)
+        for s in ("f64", "f32"):
+            getattr(self.L, f"orc_apply_box_{s}").restype = ctypes.c_int64
+            getattr(self.L, f"orc_naive_run_{s}").restype = ctypes.c_int
+        self.L.orc_mt64_stream.argtypes = [ctypes.c_uint64, ctypes.c_int64, _vp]
+
+    def mt64(self, seed: int, count: int) -> np.ndarray:
+        out = np.zeros(count, dtype=np.uint64)
+        self.L.orc_mt64_stream(ctypes.c_uint64(seed), count, out.ctypes.data)
+        return out
+
+    def fill_random(self, grid, seed: int, lo: float = 0.0, hi: float = 1.0) -> None:
+        ext, halo = _geom(grid)
+        b0, b1 = grid.c_buffers()
+        getattr(self.L, f"orc_fill_random_{_sfx(grid)}")(
+            grid.dims, ext, halo, ctypes.c_uint64(seed), ctypes.c_double(lo), ctypes.c_double(hi),
+            _vp(b0), _vp(b1))
+
+    def naive_run(self, grid, kernel, steps: int) -> None:
+        ext, halo = _geom(grid)
+        n, offs, ws = _taps(kernel)
+        b0, b1 = grid.c_buffers()
+        p = getattr(self.L, f"orc_naive_run_{_sfx(grid)}")(
+            grid.dims, ext, halo, n, offs, ws, _vp(b0), _vp(b1), grid.parity,
+            ctypes.c_int64(steps))
+        if p < 0:
+            raise ValueError("oracle naive_run rejected its arguments")
+        if p != grid.parity:
+            grid.flip_parity()
+
+    def apply_box(self, grid, kernel, lo, hi, read_parity: int) -> int:
+        """apply_box on [lo, hi) reading buffer `read_parity`; no flip."""
+        ext, halo = _geom(grid)
+        n, offs, ws = _taps(kernel)
+        lo3 = (ctypes.c_int64 * 3)(*(list(lo) + [0] * (3 - len(lo))))
+        hi3 = (ctypes.c_int64 * 3)(*(list(hi) + [1] * (3 - len(hi))))
+        bufs = grid.c_buffers()
+        return getattr(self.L, f"orc_apply_box_{_sfx(grid)}")(
+            grid.dims, ext, halo, n, offs, ws, lo3, hi3, _vp(bufs[read_parity]),
+            _vp(bufs[1 - read_parity]))
+
+    def deviation(self, a, ref) -> dict:
+        """(max_rel_deviation, max_abs, l2_rel) on the read buffers."""
+        ext, halo = _geom(ref)
+        out = (ctypes.c_double * 3)()
+        getattr(self.L, f"orc_deviation_{_sfx(ref)}")(
+            ref.dims, ext, halo, _vp(a.read_data().ctypes.data),
+            _vp(ref.read_data().ctypes.data), out)
+        return {"max_rel_deviation": out[0], "max_abs_err": out[1], "l2_rel_err": out[2]}
+
+
+class Reference:
+    """The reference library itself (oracle/_ref/libtessera_ref.so)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"reference build missing: {path} (run make -C oracle ref)")
+        self.L = ctypes.CDLL(path)
+        self.L.ref_last_error.restype = ctypes.c_char_p
+
+    @staticmethod
+    def available() -> bool:
+        return os.path.exists(REF_SO)
+
+    def _err(self, rc):
+        if rc < 0:
+            raise ValueError(self.L.ref_last_error().decode())
+        return rc
+
+    def threads(self) -> int:
+        return self.L.ref_default_threads()
+
+    def benchmark_kernel(self, name: str):
+        dims, shape, radius = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        offs = (ctypes.c_int32 * (3 * 125))()
+        ws = (ctypes.c_double * 125)()
+        n = self._err(self.L.ref_benchmark_kernel(name.encode(), ctypes.byref(dims),
+                                                  ctypes.byref(shape), ctypes.byref(radius),
+                                                  offs, ws))
+        taps = [((offs[3 * t], offs[3 * t + 1], offs[3 * t + 2]), ws[t]) for t in range(n)]
+        return dims.value, ("star", "box")[shape.value], radius.value, taps
+
+    def fill_random(self, grid, seed: int, lo: float = 0.0, hi: float = 1.0) -> None:
+        ext, halo = _geom(grid)
+        b0, b1 = grid.c_buffers()
+        self._err(getattr(self.L, f"ref_fill_random_{_sfx(grid)}")(
+            grid.dims, ext, halo, ctypes.c_uint64(seed), ctypes.c_double(lo),
+            ctypes.c_double(hi), _vp(b0), _vp(b1)))
+
+    def naive_run(self, grid, kernel, steps: int) -> None:
+        ext, halo = _geom(grid)
+        n, offs, ws = _taps(kernel)
+        b0, b1 = grid.c_buffers()
+        p = self._err(getattr(self.L, f"ref_naive_run_{_sfx(grid)}")(
+            grid.dims, ext, halo, ("star", "box").index(kernel.shape), kernel.radius, n, offs,
+            ws, _vp(b0), _vp(b1), grid.parity, ctypes.c_int64(steps)))
+        if p != grid.parity:
+            grid.flip_parity()
+
+    def run_tessellated(self, grid, kernel, steps: int, tile, tb: int, threads: int = 1):
+        """Returns ((point_updates, rounds, trailing), seconds)."""
+        ext, halo = _geom(grid)
+        n, offs, ws = _taps(kernel)
+        b0, b1 = grid.c_buffers()
+        t3 = (ctypes.c_int64 * 3)(*(list(tile) + [1] * (3 - len(tile))))
+        st = (ctypes.c_int64 * 3)()
+        sec = ctypes.c_double()
+        p = self._err(self.L.ref_run_tessellated(
+            grid.dims, ext, halo, ("star", "box").index(kernel.shape), kernel.radius, n, offs,
+            ws, _vp(b0), _vp(b1), grid.parity, ctypes.c_int64(steps), t3, tb, threads, st,
+            ctypes.byref(sec)))
+        if p != grid.parity:
+            grid.flip_parity()
+        return (st[0], st[1], st[2]), sec.value
+
+    def time_naive_f32(self, grid, kernel, steps: int) -> float:
+        ext, halo = _geom(grid)
+        n, offs, ws = _taps(kernel)
+        b0, b1 = grid.c_buffers()
+        sec = ctypes.c_double()
+        p = self._err(self.L.ref_time_naive_f32(
+            grid.dims, ext, halo, ("star", "box").index(kernel.shape), kernel.radius, n, offs,
+            ws, _vp(b0), _vp(b1), grid.parity, ctypes.c_int64(steps), ctypes.byref(sec)))
+        if p != grid.parity:
+            grid.flip_parity()
+        return sec.value
+
+    def run_heterogeneous(self, grid, kernel, steps: int, tile_width: int, tb: int,
+                          threaded: bool = False):
+        """Returns (messages, ghost_recompute_points, first_message_bytes, boundary)."""
+        ext, halo = _geom(grid)
+        n, offs, ws = _taps(kernel)
+        b0, b1 = grid.c_buffers()
+        log = (ctypes.c_int64 * 3)()
+        bnd = ctypes.c_int64()
+        p = self._err(self.L.ref_run_heterogeneous(
+            grid.dims, ext, halo, ("star", "box").index(kernel.shape), kernel.radius, n, offs,
+            ws, _vp(b0), _vp(b1), grid.parity, ctypes.c_int64(steps),
+            ctypes.c_int64(tile_width), tb, int(threaded), log, ctypes.byref(bnd)))
+        if p != grid.parity:
+            grid.flip_parity()
+        return log[0], log[1], log[2], bnd.value

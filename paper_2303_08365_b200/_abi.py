@@ -1,0 +1,155 @@
+"""ctypes binding of the C-ABI in include/tessera_b200.h.
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2303_08365_b200/csrc``) into ``paper_2303_08365_b200/_native``.
+There is no fallback: if the library is missing, every call that needs it
+raises ``ImportError`` with the build command.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_native", "libtessera_b200.so")
+
+TSR_OK, TSR_EINVAL, TSR_ECUDA, TSR_ENCCL, TSR_ENOMEM, TSR_EUNSUPPORTED = range(6)
+TSR_F64, TSR_F32 = 0, 1
+TSR_STAR, TSR_BOX = 0, 1
+TSR_EXACT, TSR_FAST = 0, 1
+ENGINES = {"auto": 0, "generic": 1, "tuned": 2}
+MODES = {"exact": TSR_EXACT, "fast": TSR_FAST}
+
+# Every symbol include/tessera_b200.h declares (tests check the .so exports them).
+EXPORTED = (
+    "tsr_abi_version", "tsr_last_error", "tsr_release_cache", "tsr_check_kernel",
+    "tsr_fill_random", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
+    "tsr_copy_halo", "tsr_advance", "tsr_apply_box",
+)
+
+
+class TsrKernel(ctypes.Structure):
+    _fields_ = [
+        ("dims", ctypes.c_int32),
+        ("shape", ctypes.c_int32),
+        ("radius", ctypes.c_int32),
+        ("ntaps", ctypes.c_int32),
+        ("offsets", ctypes.POINTER(ctypes.c_int32)),
+        ("weights", ctypes.POINTER(ctypes.c_double)),
+    ]
+
+
+class TsrGrid(ctypes.Structure):
+    _fields_ = [
+        ("dims", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("extent", ctypes.c_int64 * 3),
+        ("halo", ctypes.c_int64 * 3),
+    ]
+
+
+class TsrLayout(ctypes.Structure):
+    _fields_ = [
+        ("pitch", ctypes.c_int64 * 3),
+        ("origin", ctypes.c_int64),
+        ("elements", ctypes.c_int64),
+    ]
+
+
+class TsrOpts(ctypes.Structure):
+    _fields_ = [
+        ("fused_steps", ctypes.c_int32),
+        ("mode", ctypes.c_int32),
+        ("engine", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+    ]
+
+
+class TsrStats(ctypes.Structure):
+    _fields_ = [
+        ("device_ms", ctypes.c_double),
+        ("point_updates", ctypes.c_int64),
+        ("rounds", ctypes.c_int64),
+        ("trailing_steps", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
+        ("fused_steps", ctypes.c_int32),
+        ("engine", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> ctypes.CDLL:
+    """Loads the engine library (once); raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"B200 sweep engine not built: {LIB_PATH} is missing "
+                "(run `python -c 'import __graft_entry__ as g; g.build()'` or "
+                "`make -C paper_2303_08365_b200/csrc`)")
+        L = ctypes.CDLL(LIB_PATH)
+        p, c_void_p = ctypes.POINTER, ctypes.c_void_p
+        L.tsr_abi_version.restype = ctypes.c_int
+        L.tsr_last_error.restype = ctypes.c_char_p
+        L.tsr_release_cache.restype = ctypes.c_int
+        L.tsr_check_kernel.argtypes = [p(TsrKernel)]
+        L.tsr_fill_random.argtypes = [p(TsrGrid), c_void_p, c_void_p, ctypes.c_uint64,
+                                      ctypes.c_double, ctypes.c_double]
+        L.tsr_layout_of.argtypes = [p(TsrGrid), p(TsrLayout)]
+        L.tsr_run.argtypes = [p(TsrKernel), p(TsrGrid), c_void_p, c_void_p, ctypes.c_int32,
+                              ctypes.c_int64, p(TsrOpts), p(TsrStats)]
+        L.tsr_upload.argtypes = [p(TsrGrid), p(TsrLayout), c_void_p, c_void_p, c_void_p]
+        L.tsr_download.argtypes = [p(TsrGrid), p(TsrLayout), c_void_p, c_void_p,
+                                   ctypes.c_int32, c_void_p]
+        L.tsr_copy_halo.argtypes = [p(TsrGrid), p(TsrLayout), c_void_p, c_void_p, c_void_p]
+        L.tsr_advance.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrLayout), c_void_p, c_void_p,
+                                  p(ctypes.c_int32), ctypes.c_int64, ctypes.c_int32,
+                                  p(TsrOpts), c_void_p, p(TsrStats)]
+        L.tsr_apply_box.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrLayout), c_void_p, c_void_p,
+                                    p(ctypes.c_int64), p(ctypes.c_int64), p(TsrOpts), c_void_p]
+        for name in EXPORTED:
+            if name not in ("tsr_abi_version", "tsr_last_error"):
+                getattr(L, name).restype = ctypes.c_int
+        if L.tsr_abi_version() != 1:
+            raise ImportError("libtessera_b200.so ABI version mismatch")
+        _lib = L
+        return L
+
+
+def check(code: int) -> None:
+    """Raises the Python exception matching a tsr_status (pybind11's mapping
+    of the reference's std exceptions: invalid_argument -> ValueError)."""
+    if code == TSR_OK:
+        return
+    msg = (lib().tsr_last_error() or b"").decode(errors="replace")
+    if code == TSR_EINVAL:
+        raise ValueError(msg)
+    if code == TSR_ENOMEM:
+        raise MemoryError(msg)
+    if code == TSR_EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RuntimeError(msg)
+
+
+def make_opts(fused_steps: int = 0, mode: str = "exact", engine: str = "auto",
+              device: int = -1) -> TsrOpts:
+    if mode not in MODES:
+        raise ValueError("mode must be 'exact' or 'fast'")
+    if engine not in ENGINES:
+        raise ValueError("engine must be 'auto', 'generic' or 'tuned'")
+    if fused_steps < 0:
+        raise ValueError("fused_steps must be >= 0")
+    return TsrOpts(int(fused_steps), MODES[mode], ENGINES[engine], int(device))

@@ -1,0 +1,132 @@
+// common.cuh — shared geometry, tap tables and arithmetic modes for the
+// B200 sweep engines.
+//
+// Every grid is normalised to three axes (a0, a1, a2) with a2 contiguous:
+// a 1-D grid of extent n becomes (1, 1, n), a 2-D grid (n0, n1) becomes
+// (1, n0, n1).  Tap offsets are shifted the same way, so one set of kernels
+// serves the reference's 1-, 2- and 3-D BasicGrid<T>
+// (proj/include/tessera/grid.hpp:26-132).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include "../../include/tessera_b200.h"
+
+namespace tsr {
+
+constexpr int kMaxTaps = 1024;
+
+// Normalised geometry plus the device (pitched) layout of one buffer.
+struct Geo {
+    int dims = 0;        // the grid's own dimensionality (1..3)
+    int dtype = TSR_F64;
+    int esize = 8;       // bytes per element
+    int64_t n[3]{};      // interior extents, normalised
+    int64_t h[3]{};      // halo widths, normalised
+    int64_t pitch[3]{};  // device element strides, pitch[2] == 1
+    int64_t off2 = 0;    // element offset of interior a2 == 0 inside a row
+    int64_t origin = 0;  // element offset of interior (0,0,0)
+    int64_t elements = 0;
+    // host (reference) layout strides, grid.hpp:46-49
+    int64_t hpitch[3]{};
+    int64_t horigin = 0;
+    int64_t host_elements = 0;
+
+    int64_t interior() const { return n[0] * n[1] * n[2]; }
+    int64_t rows_padded() const { return (n[0] + 2 * h[0]) * (n[1] + 2 * h[1]); }
+};
+
+// Tap table normalised to three axes, canonical order preserved.
+struct TapSet {
+    int dims = 0;
+    int shape = TSR_STAR;
+    int radius = 0;
+    int ntaps = 0;
+    int off[kMaxTaps][3];
+    double w[kMaxTaps];
+};
+
+// Status + message, set by the host helpers; the C-ABI turns it into
+// tsr_last_error().
+struct Status {
+    int code = TSR_OK;
+    std::string msg;
+    bool ok() const { return code == TSR_OK; }
+    static Status Ok() { return {}; }
+    static Status Err(int c, std::string m) { return {c, std::move(m)}; }
+};
+
+Status make_geo(const tsr_grid& g, Geo& out);
+Status make_taps(const tsr_kernel& k, TapSet& out);
+Status check_layout(const Geo& g, const tsr_layout* l);
+
+#define TSR_CUDA_TRY(expr)                                                              \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return ::tsr::Status::Err(TSR_ECUDA, std::string(#expr) + ": " +            \
+                                                     cudaGetErrorString(_e));           \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Arithmetic modes.  EXACT reproduces `acc += w * x` of apply_box compiled
+// with -ffp-contract=off (proj/CMakeLists.txt:35-38, naive.hpp:76-78): a
+// separately rounded multiply and add, never contracted.  FAST is one FMA per
+// tap in the same order.
+// ---------------------------------------------------------------------------
+template <bool EXACT>
+__device__ __forceinline__ double madd(double acc, double w, double x) {
+    if constexpr (EXACT) {
+        return __dadd_rn(acc, __dmul_rn(w, x));
+    } else {
+        return __fma_rn(w, x, acc);
+    }
+}
+
+template <bool EXACT>
+__device__ __forceinline__ float madd(float acc, float w, float x) {
+    if constexpr (EXACT) {
+        return __fadd_rn(acc, __fmul_rn(w, x));
+    } else {
+        return __fmaf_rn(w, x, acc);
+    }
+}
+
+// First tap: apply_box starts from acc = T(0) (naive.hpp:75), so the first
+// sum is 0 + w*x, which maps -0 to +0.  Kept explicit for bitwise parity.
+template <bool EXACT, typename T>
+__device__ __forceinline__ T first(T w, T x) {
+    return madd<EXACT>(T(0), w, x);
+}
+
+// ---------------------------------------------------------------------------
+// Engine entry points (each in its own translation unit).
+// ---------------------------------------------------------------------------
+struct LaunchCtx {
+    const Geo* g;
+    const TapSet* taps;
+    bool exact;
+    cudaStream_t stream;
+};
+
+// One sweep over the normalised box [lo, hi) from `in` to `out` (apply_box).
+Status generic_sweep(const LaunchCtx& c, const void* in, void* out, const int64_t lo[3],
+                     const int64_t hi[3]);
+
+// Tuned engines.  `supports` reports whether an engine serves the kernel and
+// the largest fused step count it accepts; `run` advances `k` steps from `in`
+// to `out` in one pass over HBM (in != out).
+struct Engine {
+    const char* name;
+    bool (*supports)(const Geo&, const TapSet&, int* max_fused, int* default_fused);
+    Status (*run)(const LaunchCtx&, const void* in, void* out, int k);
+};
+const Engine* find_engine(const Geo& g, const TapSet& t, int* max_fused, int* default_fused);
+
+Status halo_copy(const Geo& g, const void* src, void* dst, cudaStream_t s);
+
+}  // namespace tsr

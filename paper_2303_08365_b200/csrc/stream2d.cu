@@ -1,0 +1,310 @@
+// stream2d.cu — 2-D star / box sweeps with K time steps fused per HBM pass.
+//
+// Register-level tetrominoes (north_star tier 1) + temporal blocking (tier 2):
+// every warp owns a strip of 32*V columns and streams down the rows.  Each
+// lane keeps, for every fused level l = 0..K-1, the last 2R+1 rows of its V
+// columns in registers; level l+1 of row x is computed as soon as level l of
+// row x+R exists, so one pass over HBM advances K time steps.  Column
+// neighbours come from the adjacent lanes through warp shuffles.  Strips
+// overlap by R*K columns per side (overlapped tiling): edge lanes compute
+// values that are never stored.
+//
+// Dirichlet semantics under fusion (proj/include/tessera/grid.hpp:14-18): a
+// cell outside the interior keeps its level-0 (halo) value at every level,
+// so a fused pass reads exactly what K separate apply_box sweeps would.
+// Interior cells sum the taps in canonical lexicographic order (dr, dc),
+// identical per point to apply_box (proj/include/tessera/naive.hpp:69-82),
+// so EXACT mode is bitwise equal to naive_run for any K.
+#include "common.cuh"
+
+namespace tsr {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+
+template <typename T>
+struct S2Args {
+    int64_t rows, cols;      // interior extents (normalised a1, a2)
+    int64_t hrow;            // halo rows (a1)
+    int64_t pitch;           // row pitch (elements)
+    int64_t origin;          // element index of interior (0,0)
+    int64_t col_lo, col_hi;  // allocated column range relative to interior col 0
+    int64_t chunk;           // output rows per warp
+    int64_t nstrips;
+    int64_t wout;            // output columns per strip
+    int64_t hl;              // left margin of the strip (>= R*K, vector aligned)
+    int64_t total_warps;
+    T w[25];
+};
+
+template <int R, bool BOX>
+__host__ __device__ constexpr bool has_tap(int dr, int dc) {
+    return BOX || dr == 0 || dc == 0;
+}
+
+template <typename T, int V>
+struct Vec;
+template <>
+struct Vec<double, 2> {
+    using type = double2;
+};
+template <>
+struct Vec<float, 4> {
+    using type = float4;
+};
+template <>
+struct Vec<double, 4> {
+    using type = double4;
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void load_row(const T* __restrict__ p, bool ok, T (&v)[V]) {
+    if (ok) {
+        if constexpr (sizeof(T) * V == 16) {
+            const auto x = __ldg(reinterpret_cast<const typename Vec<T, V>::type*>(p));
+            const T* xs = reinterpret_cast<const T*>(&x);
+#pragma unroll
+            for (int i = 0; i < V; ++i) v[i] = xs[i];
+        } else {
+#pragma unroll
+            for (int i = 0; i < V; i += 16 / (int)sizeof(T)) {
+                const uint4 x = __ldg(reinterpret_cast<const uint4*>(p + i));
+                const T* xs = reinterpret_cast<const T*>(&x);
+#pragma unroll
+                for (int q = 0; q < 16 / (int)sizeof(T); ++q) v[i + q] = xs[q];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[i] = T(0);
+    }
+}
+
+// Fills the R halo columns on each side of a row from the neighbouring lanes.
+template <typename T, int V, int R>
+__device__ __forceinline__ void exchange(T (&row)[V + 2 * R]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        row[r] = __shfl_up_sync(0xffffffffu, row[V + r], 1);          // left: lane-1's tail
+        row[V + R + r] = __shfl_down_sync(0xffffffffu, row[R + r], 1);  // right: lane+1's head
+    }
+}
+
+template <typename T, int R, bool BOX, int K, int V, bool EXACT>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
+    const T* __restrict__ in, T* __restrict__ out, const __grid_constant__ S2Args<T> a) {
+    constexpr int P = 2 * R + 1;  // ring depth per level
+    constexpr int W = V + 2 * R;  // values per ring row incl. lane halo
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = blockIdx.x * (int64_t)kWarpsPerBlock + (threadIdx.x >> 5);
+    if (gw >= a.total_warps) return;
+    const int64_t strip = gw % a.nstrips;
+    const int64_t chunk = gw / a.nstrips;
+    const int64_t rb = chunk * a.chunk;
+    const int64_t re = min(rb + a.chunk, a.rows);
+    const int64_t ob = strip * a.wout;                 // first output column
+    const int64_t oe = min(ob + a.wout, a.cols);       // output column end
+    const int64_t c0 = ob - a.hl + (int64_t)lane * V;  // this lane's first column
+    const bool col_alloc = c0 >= a.col_lo && c0 + V <= a.col_hi;
+
+    // Per-value column masks (constant down the strip).
+    bool cint[V], cout[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        cint[v] = c0 + v >= 0 && c0 + v < a.cols;
+        cout[v] = c0 + v >= ob && c0 + v < oe;
+    }
+    bool all_out = true;
+#pragma unroll
+    for (int v = 0; v < V; ++v) all_out &= cout[v];
+
+    T win[K][P][W];  // ring of rows per level (level K is stored, not kept)
+    T pf[P][V];      // prefetch ring of level-0 rows
+
+    const int64_t t_start = rb - (int64_t)K * R;
+    const int64_t t_end = re + (int64_t)K * R;  // exclusive
+    const T* base_in = in + a.origin + c0;
+    T* base_out = out + a.origin + c0;
+
+    auto row_ok = [&](int64_t r) { return r >= -a.hrow && r < a.rows + a.hrow && col_alloc; };
+
+    // Prime the prefetch ring with rows t_start .. t_start+P-1.
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+        const int64_t r = t_start + s;
+        load_row<T, V>(base_in + r * a.pitch, row_ok(r), pf[s]);
+    }
+
+    for (int64_t tb = t_start; tb < t_end; tb += P) {
+#pragma unroll
+        for (int ph = 0; ph < P; ++ph) {
+            const int64_t t = tb + ph;
+            if (t < t_end) {
+                // Level 0: take row t from the prefetch ring, refill the slot.
+#pragma unroll
+                for (int v = 0; v < V; ++v) win[0][ph][R + v] = pf[ph][v];
+                {
+                    const int64_t r = t + P;
+                    load_row<T, V>(base_in + r * a.pitch, row_ok(r) && r < t_end, pf[ph]);
+                }
+                if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
+
+                // Levels 1..K: level l produces row x = t - l*R.
+#pragma unroll
+                for (int l = 1; l <= K; ++l) {
+                    const int64_t x = t - (int64_t)l * R;
+                    const int sx = ((ph - l * R) % P + P) % P;  // slot of row x (static)
+                    const bool rint = x >= 0 && x < a.rows;
+                    // Star taps read lane-halo columns of the centre row only:
+                    // exchange it at use, so the halos of the other rows never
+                    // occupy registers.  Box rows carry halos from production.
+                    if constexpr (!BOX) exchange<T, V, R>(win[l - 1][sx]);
+                    T res[V];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        T acc = T(0);
+                        int tap = 0;
+#pragma unroll
+                        for (int dr = -R; dr <= R; ++dr) {
+                            const int sr = ((sx + dr) % P + P) % P;
+#pragma unroll
+                            for (int dc = -R; dc <= R; ++dc) {
+                                if (has_tap<R, BOX>(dr, dc)) {
+                                    const T xv = win[l - 1][sr][R + v + dc];
+                                    acc = tap == 0 ? first<EXACT>(a.w[0], xv)
+                                                   : madd<EXACT>(acc, a.w[tap], xv);
+                                    ++tap;
+                                }
+                            }
+                        }
+                        const T keep = win[l - 1][sx][R + v];
+                        res[v] = (rint && cint[v]) ? acc : keep;
+                    }
+                    if (l < K) {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) win[l][sx][R + v] = res[v];
+                        if constexpr (BOX) exchange<T, V, R>(win[l][sx]);
+                    } else if (x >= rb && x < re) {
+                        T* dst = base_out + x * a.pitch;
+                        if (all_out) {
+                            if constexpr (sizeof(T) * V == 16) {
+                                typename Vec<T, V>::type o;
+                                T* os = reinterpret_cast<T*>(&o);
+#pragma unroll
+                                for (int v = 0; v < V; ++v) os[v] = res[v];
+                                *reinterpret_cast<typename Vec<T, V>::type*>(dst) = o;
+                            } else {
+#pragma unroll
+                                for (int v = 0; v < V; ++v) dst[v] = res[v];
+                            }
+                        } else {
+#pragma unroll
+                            for (int v = 0; v < V; ++v)
+                                if (cout[v]) dst[v] = res[v];
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+struct Shape {
+    int R;
+    bool box;
+};
+
+bool classify(const TapSet& t, Shape* s) {
+    if (t.dims != 2) return false;
+    if (t.shape == TSR_STAR && (t.radius == 1 || t.radius == 2)) {
+        *s = {t.radius, false};
+        return true;
+    }
+    if (t.shape == TSR_BOX && t.radius == 1) {
+        *s = {1, true};
+        return true;
+    }
+    return false;
+}
+
+constexpr int kMaxK = 8;
+
+bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
+    Shape s;
+    if (!classify(t, &s)) return false;
+    *max_fused = kMaxK;
+    *default_fused = 4;
+    return true;
+}
+
+template <typename T, int R, bool BOX, int K, int V>
+Status launch_k(const LaunchCtx& c, const void* in, void* out) {
+    const Geo& g = *c.g;
+    S2Args<T> a;
+    a.rows = g.n[1];
+    a.cols = g.n[2];
+    a.hrow = g.h[1];
+    a.pitch = g.pitch[1];
+    a.origin = g.origin;
+    a.col_lo = -g.off2;
+    a.col_hi = g.pitch[1] - g.off2;
+    constexpr int vec = 16 / sizeof(T);
+    a.hl = ((int64_t)R * K + vec - 1) / vec * vec;
+    a.wout = (32 * V - a.hl - (int64_t)R * K) / vec * vec;
+    if (a.wout <= 0) return Status::Err(TSR_EUNSUPPORTED, "stream2d: strip too narrow for K");
+    a.nstrips = (a.cols + a.wout - 1) / a.wout;
+    // Aim for ~16 resident warps per SM, chunks of >= 16*K*R rows.
+    const int64_t target = 148 * 24;
+    int64_t nchunks = std::max<int64_t>(1, target / a.nstrips);
+    a.chunk = std::max<int64_t>(16 * K * R, (a.rows + nchunks - 1) / nchunks);
+    nchunks = (a.rows + a.chunk - 1) / a.chunk;
+    a.total_warps = nchunks * a.nstrips;
+    for (int t = 0; t < c.taps->ntaps; ++t) a.w[t] = static_cast<T>(c.taps->w[t]);
+    const unsigned blocks =
+        static_cast<unsigned>((a.total_warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    if (c.exact)
+        stream2d_kernel<T, R, BOX, K, V, true><<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
+            static_cast<const T*>(in), static_cast<T*>(out), a);
+    else
+        stream2d_kernel<T, R, BOX, K, V, false><<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
+            static_cast<const T*>(in), static_cast<T*>(out), a);
+    TSR_CUDA_TRY(cudaGetLastError());
+    return Status::Ok();
+}
+
+template <typename T, int R, bool BOX>
+Status launch_shape(const LaunchCtx& c, const void* in, void* out, int k) {
+    constexpr int V = 16 / sizeof(T);  // one 16-byte vector per lane per row
+    switch (k) {
+        case 1: return launch_k<T, R, BOX, 1, V>(c, in, out);
+        case 2: return launch_k<T, R, BOX, 2, V>(c, in, out);
+        case 3: return launch_k<T, R, BOX, 3, V>(c, in, out);
+        case 4: return launch_k<T, R, BOX, 4, V>(c, in, out);
+        case 5: return launch_k<T, R, BOX, 5, V>(c, in, out);
+        case 6: return launch_k<T, R, BOX, 6, V>(c, in, out);
+        case 7: return launch_k<T, R, BOX, 7, V>(c, in, out);
+        case 8: return launch_k<T, R, BOX, 8, V>(c, in, out);
+        default: return Status::Err(TSR_EUNSUPPORTED, "stream2d: fused steps must be 1..8");
+    }
+}
+
+template <typename T>
+Status launch_t(const LaunchCtx& c, const void* in, void* out, int k) {
+    Shape s;
+    classify(*c.taps, &s);
+    if (s.box) return launch_shape<T, 1, true>(c, in, out, k);
+    if (s.R == 1) return launch_shape<T, 1, false>(c, in, out, k);
+    return launch_shape<T, 2, false>(c, in, out, k);
+}
+
+Status run(const LaunchCtx& c, const void* in, void* out, int k) {
+    if (c.g->dtype == TSR_F64) return launch_t<double>(c, in, out, k);
+    return launch_t<float>(c, in, out, k);
+}
+
+}  // namespace
+
+extern const Engine kStream2dEngine = {"stream2d_regtile", supports, run};
+
+}  // namespace tsr

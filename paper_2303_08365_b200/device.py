@@ -1,0 +1,109 @@
+"""Device-resident grids: the two buffers of a BasicGrid<T> living in HBM in
+the engine's pitched layout (``tsr_layout_of``), advanced without host
+round trips.  torch supplies the device memory and streams (plumbing only);
+every sweep is a launch of the engine library through ``tsr_advance``.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _abi
+from .grid import BasicGrid
+from .kernel import StencilKernel
+
+
+def layout_of(grid_desc: _abi.TsrGrid) -> _abi.TsrLayout:
+    L = _abi.lib()
+    lay = _abi.TsrLayout()
+    _abi.check(L.tsr_layout_of(ctypes.byref(grid_desc), ctypes.byref(lay)))
+    return lay
+
+
+def _torch_dtype(grid: BasicGrid):
+    import torch
+    return torch.float64 if grid._tsr_dtype == _abi.TSR_F64 else torch.float32
+
+
+class DeviceGrid:
+    """Device copy of a host grid.  ``advance`` runs fused sweeps on the
+    current torch stream; ``download`` writes the state back into a host grid
+    exactly as naive_run would have left it."""
+
+    def __init__(self, grid: BasicGrid, device=None, *, upload: bool = True):
+        import torch
+        self.torch = torch
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.type != "cuda":
+            raise ValueError("DeviceGrid needs a CUDA device")
+        self.desc = grid.c_struct()
+        self.layout = layout_of(self.desc)
+        self.dims = grid.dims
+        self.extent = grid.extent
+        self.halo = grid.halo
+        self.esize = 8 if grid._tsr_dtype == _abi.TSR_F64 else 4
+        n = self.layout.elements
+        self.buf = [torch.empty(n, dtype=_torch_dtype(grid), device=self.device),
+                    torch.empty(n, dtype=_torch_dtype(grid), device=self.device)]
+        self.cur = 0
+        self.steps_done = 0
+        self.prev_valid = False
+        if upload:
+            self.upload(grid)
+
+    def _stream(self, stream=None) -> int:
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        return s.cuda_stream
+
+    def ptr(self, which: int) -> int:
+        return self.buf[which].data_ptr()
+
+    def upload(self, grid: BasicGrid, stream=None) -> None:
+        """Read buffer of `grid` -> device buffer 0, halo shell -> buffer 1."""
+        L = _abi.lib()
+        s = self._stream(stream)
+        with self.torch.cuda.device(self.device):
+            _abi.check(L.tsr_upload(ctypes.byref(self.desc), ctypes.byref(self.layout),
+                                    grid.read_data().ctypes.data, self.ptr(0), s))
+            _abi.check(L.tsr_copy_halo(ctypes.byref(self.desc), ctypes.byref(self.layout),
+                                       self.ptr(0), self.ptr(1), s))
+        self.cur = 0
+        self.steps_done = 0
+        self.prev_valid = False
+
+    def advance(self, kernel: StencilKernel, steps: int, *, fused_steps: int = 0,
+                mode: str = "exact", engine: str = "auto", keep_previous: bool = False,
+                stream=None) -> _abi.TsrStats:
+        L = _abi.lib()
+        st = _abi.TsrStats()
+        cur = ctypes.c_int32(self.cur)
+        opts = _abi.make_opts(fused_steps, mode, engine)
+        with self.torch.cuda.device(self.device):
+            _abi.check(L.tsr_advance(ctypes.byref(kernel.c_struct()), ctypes.byref(self.desc),
+                                     ctypes.byref(self.layout), self.ptr(0), self.ptr(1),
+                                     ctypes.byref(cur), int(steps), int(bool(keep_previous)),
+                                     ctypes.byref(opts), self._stream(stream),
+                                     ctypes.byref(st)))
+        self.cur = cur.value
+        if steps > 0:
+            # One step (or keep_previous) leaves step T-1 in the other buffer.
+            self.prev_valid = bool(keep_previous) or steps == 1
+        self.steps_done += int(steps)
+        return st
+
+    def download(self, grid: BasicGrid, stream=None) -> None:
+        """Interior of the current buffer -> grid.buffer(final parity); the
+        previous step (when kept) -> the other buffer; parity flipped by the
+        number of steps advanced since upload."""
+        L = _abi.lib()
+        s = self._stream(stream)
+        if self.steps_done & 1:
+            grid.flip_parity()
+        bufs = grid.c_buffers()
+        with self.torch.cuda.device(self.device):
+            _abi.check(L.tsr_download(ctypes.byref(self.desc), ctypes.byref(self.layout),
+                                      self.ptr(self.cur), bufs[grid.parity], 1, s))
+            if self.steps_done >= 1 and self.prev_valid:
+                _abi.check(L.tsr_download(ctypes.byref(self.desc), ctypes.byref(self.layout),
+                                          self.ptr(1 - self.cur), bufs[1 - grid.parity], 1, s))
+            self.torch.cuda.current_stream(self.device).synchronize()
+        self.steps_done = 0

@@ -1,0 +1,218 @@
+"""GPU parity: every engine against the CPU oracle (pinned in test_oracle.py)
+and the reference's golden fixtures.  EXACT mode must be bitwise equal;
+FAST mode within the north star's tolerances (1e-12 fp64, 1e-5 fp32, as
+max-rel / L2-rel after N steps)."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import (GOLDEN, bitwise_equal_interior, golden_index, load_golden, random_grid)
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-12, "f32": 1e-5}
+
+
+def both_buffers_equal(a, b):
+    return (a.parity == b.parity and
+            a.interior_view(0).tobytes() == b.interior_view(0).tobytes() and
+            a.interior_view(1).tobytes() == b.interior_view(1).tobytes())
+
+
+def halos_equal(a, b):
+    mask = np.ones(a.padded(0).shape, bool)
+    mask[tuple(slice(h, h + e) for e, h in zip(a.extent, a.halo))] = False
+    return all(a.padded(w)[mask].tobytes() == b.padded(w)[mask].tobytes() for w in (0, 1))
+
+
+@pytest.mark.parametrize("engine", ["auto", "generic"])
+@pytest.mark.parametrize("name", sorted(golden_index()))
+def test_golden_fixtures(ts, orc, name, engine):
+    meta = golden_index()[name]
+    cur, prev = load_golden(name)
+    k = ts.find_benchmark(meta["benchmark"]).kernel
+    g = random_grid(ts, orc, meta["extent"], meta["halo"], meta["seed"], meta["dtype"])
+    ts.run_gpu(g, k, meta["steps"], engine=engine)
+    assert g.parity == meta["final_parity"]
+    assert g.interior_view(g.parity).tobytes() == cur.tobytes()
+    assert g.interior_view(1 - g.parity).tobytes() == prev.tobytes()
+
+
+def test_golden_star2d9p_ttrs(ts, orc):
+    golden = ts.load_grid(os.path.join(GOLDEN, "star2d9p_64x64_t12.ttrs"))
+    g = random_grid(ts, orc, [64, 64], [2, 2], 42)
+    ts.naive_run(g, ts.find_benchmark("Star-2D9P").kernel, 12)
+    assert bitwise_equal_interior(g, golden)
+
+
+@pytest.mark.parametrize("name", ["Heat-2D", "Box-2D9P", "Star-2D9P"])
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_fused_2d_bitwise_all_k(ts, orc, name, dt):
+    """Every fused step count 1..8, T not a multiple of k, ragged extents
+    (narrower than one strip, wider than several), halo wider than r."""
+    k = ts.find_benchmark(name).kernel
+    rng = np.random.default_rng(7)
+    for fused in range(1, 9):
+        for extent in ([int(rng.integers(5, 40)), int(rng.integers(5, 30))],
+                       [int(rng.integers(60, 130)), int(rng.integers(100, 300))]):
+            halo = [k.radius + int(rng.integers(0, 2)), k.radius + int(rng.integers(0, 3))]
+            extent = [max(e, 2 * h + 1) for e, h in zip(extent, halo)]
+            steps = int(rng.integers(fused, 3 * fused + 2))
+            a = random_grid(ts, orc, extent, halo, fused * 31 + extent[0], dt)
+            b = a.copy()
+            st = ts.run_gpu(a, k, steps, fused_steps=fused, engine="tuned")
+            orc.naive_run(b, k, steps)
+            assert st.fused_steps == fused
+            assert both_buffers_equal(a, b), (fused, extent, halo, steps)
+            assert halos_equal(a, b)
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_heat3d_tuned_bitwise(ts, orc, dt):
+    k = ts.find_benchmark("Heat-3D").kernel
+    for extent, halo, steps in [([17, 13, 35], [1, 1, 1], 5), ([40, 33, 70], [2, 1, 3], 4),
+                                ([3, 3, 3], [1, 1, 1], 3)]:
+        a = random_grid(ts, orc, extent, halo, sum(extent), dt)
+        b = a.copy()
+        st = ts.run_gpu(a, k, steps, engine="tuned")
+        orc.naive_run(b, k, steps)
+        assert st.engine == "tuned"
+        assert both_buffers_equal(a, b), (extent, steps)
+
+
+@pytest.mark.parametrize("name", ["Heat-1D", "Star-1D5P", "Box-2D25P", "Box-3D27P"])
+def test_generic_engine_bitwise(ts, orc, name):
+    k = ts.find_benchmark(name).kernel
+    ext = {1: [301], 2: [37, 41], 3: [11, 19, 23]}[k.dims]
+    a = random_grid(ts, orc, ext, [k.radius] * k.dims, 5)
+    b = a.copy()
+    ts.naive_run(a, k, 6)
+    orc.naive_run(b, k, 6)
+    assert both_buffers_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["Heat-2D", "Box-2D9P", "Heat-3D", "Box-3D27P"])
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_fast_mode_within_tolerance(ts, orc, name, dt):
+    k = ts.find_benchmark(name).kernel
+    ext = [96, 130] if k.dims == 2 else [20, 24, 40]
+    a = random_grid(ts, orc, ext, [1] * k.dims, 3, dt)
+    b = a.copy()
+    ts.run_gpu(a, k, 40, mode="fast")
+    orc.naive_run(b, k, 40)
+    d = ts.deviation(a, b)
+    assert d["max_rel_deviation"] <= TOL[dt] and d["l2_rel_err"] <= TOL[dt], d
+
+
+def test_step_counts_and_postconditions(ts, orc):
+    """T = 0, 1, 2 and odd/even T leave parity and both buffers as naive_run."""
+    k = ts.heat_coefficients(0.23)
+    for steps in (0, 1, 2, 3, 8, 9):
+        a = random_grid(ts, orc, [50, 70], [1, 1], steps)
+        b = a.copy()
+        ts.naive_run(a, k, steps)
+        orc.naive_run(b, k, steps)
+        assert both_buffers_equal(a, b), steps
+        assert halos_equal(a, b)
+
+
+def test_nonzero_dirichlet_halo(ts, orc):
+    """Halo values other than zero are read, never written, at every fused level."""
+    rng = np.random.default_rng(1)
+    for name, shape in [("Heat-2D", (45, 67)), ("Box-2D9P", (45, 67)), ("Heat-3D", (9, 14, 40))]:
+        k = ts.find_benchmark(name).kernel
+        a = ts.grid_from_numpy(rng.random(shape), halo=[2] * len(shape), halo_value=3.5)
+        b = a.copy()
+        ts.run_gpu(a, k, 7, fused_steps=4)
+        orc.naive_run(b, k, 7)
+        assert both_buffers_equal(a, b) and halos_equal(a, b)
+
+
+def test_run_tessellated_drop_in(ts, orc):
+    """tests/python/test_smoke.py:49-61 on the GPU path."""
+    rng = np.random.default_rng(7)
+    field = rng.random((32, 32))
+    k = ts.heat_coefficients(0.22)
+    a = ts.grid_from_numpy(field, halo=[1, 1])
+    b = ts.grid_from_numpy(field, halo=[1, 1])
+    plan = ts.plan_tiles([32, 32], [8, 8], 3, 1)
+    updates, rounds, trailing = ts.run_tessellated(a, k, 7, plan)
+    orc.naive_run(b, k, 7)
+    assert updates == 32 * 32 * 7 and (rounds, trailing) == (2, 1)
+    assert ts.max_rel_deviation(a, b) <= 1e-12
+    assert bitwise_equal_interior(a, b)
+
+
+def test_device_grid_roundtrip(ts, orc):
+    k = ts.find_benchmark("Box-2D9P").kernel
+    a = random_grid(ts, orc, [130, 250], [1, 1], 11)
+    b = a.copy()
+    dg = ts.DeviceGrid(a)
+    dg.advance(k, 5, fused_steps=4)
+    dg.advance(k, 6, fused_steps=3, keep_previous=True)
+    dg.download(a)
+    orc.naive_run(b, k, 11)
+    assert both_buffers_equal(a, b)
+
+
+def test_apply_box_on_device(ts, orc):
+    import ctypes
+    import torch
+    from paper_2303_08365_b200 import _abi
+    k = ts.find_benchmark("Heat-3D").kernel
+    a = random_grid(ts, orc, [12, 10, 20], [1, 1, 1], 2)
+    b = a.copy()
+    dg = ts.DeviceGrid(a)
+    lo = (ctypes.c_int64 * 3)(3, -2, 4)
+    hi = (ctypes.c_int64 * 3)(9, 7, 99)
+    L = _abi.lib()
+    _abi.check(L.tsr_apply_box(ctypes.byref(k.c_struct()), ctypes.byref(dg.desc),
+                               ctypes.byref(dg.layout), dg.ptr(0), dg.ptr(1), lo, hi, None,
+                               torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    got = a.copy()
+    L.tsr_download(ctypes.byref(dg.desc), ctypes.byref(dg.layout), dg.ptr(1),
+                   got.buffer(1).ctypes.data, 1, None)
+    n = orc.apply_box(b, k, [3, -2, 4], [9, 7, 99], 0)
+    assert n == 6 * 7 * 16
+    box = (slice(1 + 3, 1 + 9), slice(1, 1 + 7), slice(1 + 4, 1 + 20))
+    assert got.padded(1)[box].tobytes() == b.padded(1)[box].tobytes()
+
+
+@pytest.mark.slow
+def test_config1_full_size_bitwise(ts, orc):
+    """BASELINE config 1 at full size: Heat-2D 4096^2 fp64, T=100, seed 1."""
+    k = ts.find_benchmark("Heat-2D").kernel
+    a = ts.Grid([4096, 4096], [1, 1])
+    ts.fill_random(a, 1)
+    b = a.copy()
+    ts.naive_run(a, k, 100)
+    orc.naive_run(b, k, 100)
+    assert both_buffers_equal(a, b)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_full_shape_properties(ts, orc, cfg):
+    """Full BASELINE shapes: tuned engine == generic engine bitwise (exact), and
+    the first steps == the oracle; C4's fp32 fast mode within 1e-5."""
+    name, ext, dt, steps, fused = {
+        "c2": ("Box-2D9P", [16384, 16384], "f64", 8, 4),
+        "c3": ("Heat-3D", [512, 512, 512], "f64", 20, 0),
+        "c4": ("Box-3D27P", [512, 512, 512], "f32", 6, 0),
+    }[cfg]
+    k = ts.find_benchmark(name).kernel
+    cls = ts.Grid if dt == "f64" else ts.GridF
+    a = cls(ext, [1] * len(ext))
+    ts.fill_random(a, 1)
+    b = a.copy()
+    ts.run_gpu(a, k, steps, fused_steps=fused)
+    ts.run_gpu(b, k, steps, engine="generic")
+    assert both_buffers_equal(a, b)
+    c = cls(ext, [1] * len(ext))
+    ts.fill_random(c, 1)
+    d = c.copy()
+    ts.run_gpu(c, k, 2, fused_steps=fused, mode="exact")
+    orc.naive_run(d, k, 2)
+    assert both_buffers_equal(c, d)
