@@ -142,6 +142,10 @@ int tsr_copy_halo(const tsr_grid* g, const tsr_layout* l, const void* src, void*
 int tsr_advance(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, void* dev0,
                 void* dev1, int32_t* cur, int64_t steps, int32_t keep_previous,
                 const tsr_opts* opts, void* stream, tsr_stats* stats);
+/* Reports the engine (tsr_engine) and fused step count k tsr_advance /
+ * tsr_run would use for this kernel, grid and opts (no device work). */
+int tsr_query_plan(const tsr_kernel* k, const tsr_grid* g, const tsr_opts* opts,
+                   int32_t* engine, int32_t* fused_steps);
 /* One sweep of the box [lo, hi) (interior coordinates, clipped) from `in` to
  * `out`: apply_box (naive.hpp:41-84) on device buffers. */
 int tsr_apply_box(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, const void* in,

@@ -25,7 +25,7 @@ MODES = {"exact": TSR_EXACT, "fast": TSR_FAST}
 EXPORTED = (
     "tsr_abi_version", "tsr_last_error", "tsr_release_cache", "tsr_check_kernel",
     "tsr_fill_random", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
-    "tsr_copy_halo", "tsr_advance", "tsr_apply_box",
+    "tsr_copy_halo", "tsr_advance", "tsr_query_plan", "tsr_apply_box",
 )
 
 
@@ -118,6 +118,8 @@ def lib() -> ctypes.CDLL:
         L.tsr_advance.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrLayout), c_void_p, c_void_p,
                                   p(ctypes.c_int32), ctypes.c_int64, ctypes.c_int32,
                                   p(TsrOpts), c_void_p, p(TsrStats)]
+        L.tsr_query_plan.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrOpts), p(ctypes.c_int32),
+                                     p(ctypes.c_int32)]
         L.tsr_apply_box.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrLayout), c_void_p, c_void_p,
                                     p(ctypes.c_int64), p(ctypes.c_int64), p(TsrOpts), c_void_p]
         for name in EXPORTED:
@@ -153,3 +155,24 @@ def make_opts(fused_steps: int = 0, mode: str = "exact", engine: str = "auto",
     if fused_steps < 0:
         raise ValueError("fused_steps must be >= 0")
     return TsrOpts(int(fused_steps), MODES[mode], ENGINES[engine], int(device))
+
+
+def query_plan(kernel, grid_desc: TsrGrid, fused_steps: int = 0, mode: str = "exact",
+               engine: str = "auto") -> tuple[str, int]:
+    """(engine, k) the library would use for this kernel and grid."""
+    L = lib()
+    e, k = ctypes.c_int32(), ctypes.c_int32()
+    opts = make_opts(fused_steps, mode, engine)
+    check(L.tsr_query_plan(ctypes.byref(kernel.c_struct()), ctypes.byref(grid_desc),
+                           ctypes.byref(opts), ctypes.byref(e), ctypes.byref(k)))
+    return {1: "generic", 2: "tuned"}[e.value], k.value
+
+
+def grid_desc(extent, halo, dtype: str = "f64") -> TsrGrid:
+    g = TsrGrid()
+    g.dims = len(extent)
+    g.dtype = TSR_F64 if dtype == "f64" else TSR_F32
+    for a in range(3):
+        g.extent[a] = int(extent[a]) if a < len(extent) else 1
+        g.halo[a] = int(halo[a]) if a < len(extent) else 0
+    return g

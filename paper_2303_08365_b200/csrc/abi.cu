@@ -553,6 +553,23 @@ int tsr_advance(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, voi
     return report(s);
 }
 
+int tsr_query_plan(const tsr_kernel* k, const tsr_grid* g, const tsr_opts* opts,
+                   int32_t* engine, int32_t* fused_steps) {
+    if (!k || !g || !engine || !fused_steps)
+        return report(Status::Err(TSR_EINVAL, "null argument"));
+    Geo geo;
+    Status s = make_geo(*g, geo);
+    TapSet t;
+    if (s.ok()) s = make_taps(*k, t);
+    if (s.ok()) s = check_applicable(geo, t);
+    Plan p;
+    if (s.ok()) s = plan_for(geo, t, opts_or_default(opts), p);
+    if (!s.ok()) return report(s);
+    *engine = p.engine ? TSR_ENGINE_TUNED : TSR_ENGINE_GENERIC;
+    *fused_steps = p.k;
+    return TSR_OK;
+}
+
 int tsr_apply_box(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, const void* in,
                   void* out, const int64_t* lo, const int64_t* hi, const tsr_opts* opts,
                   void* stream) {

@@ -1,0 +1,271 @@
+"""Memory-level tetrominoes: 1-D slab decomposition of axis 0 over the GPUs of
+one box, with deep halos exchanged once per round of k fused steps.
+
+This generalises the reference's two-worker deep-halo partition
+(proj/src/scheduler.cpp:108-140 plan_partition, :201-435 HaloWorker,
+:441-554 run_heterogeneous_impl) to P equal slabs, GPU-only (the paper's
+CPU+GPU ratio split is out of scope per the north star):
+
+* halo depth = r * k (scheduler.cpp:123), so one exchange per k-step round
+  suffices; ghost rows are recomputed redundantly, the result is unchanged;
+* per round each seam carries one message per direction
+  (scheduler.cpp:371-406): a rank sends its first / last `depth` own planes
+  and receives its neighbours' into its ghost planes;
+* axis-0 planes are contiguous in both the host and the device layout, so a
+  slab message is a zero-copy view of the grid buffer (no pack kernels);
+* on the GPU the exchange is NCCL point-to-point (torch.distributed
+  batch_isend_irecv over NVLink/NVSwitch); the same protocol runs on gloo +
+  CPU tensors in the tests, with the oracle as the step engine.
+
+Seam-side halo planes of a local slab are beyond the ghost region and never
+influence owned rows; ``poison=True`` fills them with NaN to prove it (the
+reference's run_heterogeneous_instrumented, scheduler.cpp:410-421).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class SlabPlan:
+    """PartitionPlan (scheduler.hpp:49-64) for one rank of P equal slabs."""
+    world: int
+    rank: int
+    global_extent: list
+    halo: list
+    radius: int
+    fused_steps: int
+    depth: int          # halo depth r*k (PartitionPlan::halo_depth)
+    own_lo: int         # first owned global row (axis 0)
+    own_hi: int         # one past the last owned row
+    ghost_lo: int       # ghost rows below (0 on rank 0)
+    ghost_hi: int       # ghost rows above (0 on the last rank)
+    bytes_per_message: int = 0
+
+    @property
+    def own(self) -> int:
+        return self.own_hi - self.own_lo
+
+    @property
+    def local_extent(self) -> list:
+        return [self.ghost_lo + self.own + self.ghost_hi] + list(self.global_extent[1:])
+
+    def local_row(self, global_row: int) -> int:
+        return global_row - self.own_lo + self.ghost_lo
+
+
+def plan_slabs(global_extent, radius: int, fused_steps: int, world: int, rank: int,
+               halo=None, esize: int = 8) -> SlabPlan:
+    global_extent = [int(e) for e in global_extent]
+    halo = [radius] * len(global_extent) if halo is None else [int(h) for h in halo]
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    if fused_steps < 1:
+        raise ValueError("fused_steps must be >= 1")
+    n0 = global_extent[0]
+    base, extra = divmod(n0, world)
+    own_lo = rank * base + min(rank, extra)
+    own_hi = own_lo + base + (1 if rank < extra else 0)
+    depth = radius * fused_steps
+    if world > 1 and base < depth:
+        raise ValueError("subdomain smaller than the halo depth")  # scheduler.cpp:454
+    ghost_lo = depth if rank > 0 else 0
+    ghost_hi = depth if rank < world - 1 else 0
+    cross = 1
+    for e in global_extent[1:]:
+        cross *= e
+    return SlabPlan(world, rank, global_extent, halo, radius, fused_steps, depth, own_lo,
+                    own_hi, ghost_lo, ghost_hi, depth * cross * esize)
+
+
+def local_from_global(global_grid, plan: SlabPlan, poison: bool = False):
+    """Host local slab: owned rows + ghost rows (+ global halo at the true
+    ends) copied from a global host grid (HaloWorker::copy_from_global,
+    scheduler.cpp:236-262)."""
+    h0 = plan.halo[0]
+    loc = type(global_grid)(plan.local_extent, plan.halo)
+    g0 = plan.own_lo - plan.ghost_lo  # global row of local row 0
+    for w in (0, 1):
+        src = global_grid.padded(w)
+        dst = loc.padded(w)
+        for lr in range(-h0, plan.local_extent[0] + h0):
+            gr = g0 + lr
+            seam_halo = ((lr < 0 and plan.rank > 0) or
+                         (lr >= plan.local_extent[0] and plan.rank < plan.world - 1))
+            if seam_halo:
+                dst[lr + h0] = np.nan if poison else 0.0
+            elif -h0 <= gr < global_grid.extent[0] + h0:
+                dst[lr + h0] = src[gr + h0]
+    if global_grid.parity:
+        loc.flip_parity()
+    return loc
+
+
+@dataclass
+class CommRecord:
+    """scheduler.hpp:75-81."""
+    round: int
+    direction: str
+    bytes: int
+
+
+@dataclass
+class CommLog:
+    records: list = field(default_factory=list)
+    ghost_recompute_points: int = 0
+
+
+class _DeviceState:
+    """Local slab in HBM, stepped by the engine library (tsr_advance)."""
+
+    def __init__(self, ts, kernel, host_local, device, fused_steps, mode):
+        self.ts = ts
+        self.kernel = kernel
+        self.dg = ts.DeviceGrid(host_local, device)
+        self.fused_steps = fused_steps
+        self.mode = mode
+        self.h0 = host_local.halo[0]
+        self.plane = self.dg.layout.pitch[0] if len(host_local.extent) > 1 else 1
+
+    def advance(self, n):
+        return self.dg.advance(self.kernel, n, fused_steps=self.fused_steps, mode=self.mode)
+
+    def planes(self, row: int, count: int):
+        """Contiguous view of local planes [row, row+count) of the current buffer."""
+        start = (row + self.h0) * self.plane
+        return self.dg.buf[self.dg.cur][start:start + count * self.plane]
+
+
+class _HostState:
+    """Local slab on the host stepped by an injected CPU engine (tests only:
+    the product never steps on the CPU)."""
+
+    def __init__(self, host_local, step_fn):
+        import torch
+        self.torch = torch
+        self.g = host_local
+        self.step_fn = step_fn
+        self.h0 = host_local.halo[0]
+        self.plane = host_local.stride(0) if host_local.dims > 1 else 1
+
+    def advance(self, n):
+        self.step_fn(self.g, n)
+
+        class _S:
+            kernel_launches = 0
+        return _S()
+
+    def planes(self, row: int, count: int):
+        start = (row + self.h0) * self.plane
+        return self.torch.from_numpy(self.g.read_data()[start:start + count * self.plane])
+
+
+class SlabRunner:
+    """Round driver for one rank (HaloWorker::run_round generalised to P
+    slabs).  ``advance(n)`` runs one round of n <= k steps: exchange the
+    ghost planes with both neighbours, then n fused steps on the local slab."""
+
+    def __init__(self, plan: SlabPlan, state, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.plan = plan
+        self.state = state
+        self.group = group
+        self.fused_steps = plan.fused_steps
+        self.round = 0
+        self.log = CommLog()
+        self.exchange_bytes = 0
+
+    # -- constructors -----------------------------------------------------
+    @classmethod
+    def on_device(cls, ts, kernel, plan: SlabPlan, host_local, device, mode="exact",
+                  group=None):
+        return cls(plan, _DeviceState(ts, kernel, host_local, device, plan.fused_steps, mode),
+                   group)
+
+    @classmethod
+    def synthetic(cls, ts, kernel, plan: SlabPlan, dtype, device, seed=1, fused_steps=None,
+                  mode="exact", group=None):
+        """Benchmark slab: the local grid is filled with fill_random(seed)
+        directly (no global host grid); the first exchange makes the ghost
+        planes consistent with the neighbours."""
+        from . import _abi
+        cls_ = ts.Grid if dtype == "f64" else ts.GridF
+        # resolve the engine's k on the local geometry
+        desc = _abi.grid_desc(plan.local_extent, plan.halo, dtype)
+        _, k = _abi.query_plan(kernel, desc, fused_steps or 0, mode)
+        if k != plan.fused_steps:
+            esize = 8 if dtype == "f64" else 4
+            plan = plan_slabs(plan.global_extent, plan.radius, k, plan.world, plan.rank,
+                              plan.halo, esize)
+        host = cls_(plan.local_extent, plan.halo)
+        ts.fill_random(host, seed)
+        return cls.on_device(ts, kernel, plan, host, device, mode, group)
+
+    @classmethod
+    def on_host(cls, plan: SlabPlan, host_local, step_fn, group=None):
+        return cls(plan, _HostState(host_local, step_fn), group)
+
+    # -- protocol ---------------------------------------------------------
+    def exchange(self):
+        """One message per direction per seam (scheduler.cpp:371-381)."""
+        p, dist = self.plan, self.dist
+        d = p.depth
+        ops = []
+        if p.rank > 0:
+            ops.append(dist.P2POp(dist.isend, self.state.planes(p.ghost_lo, d), p.rank - 1,
+                                  self.group))
+            ops.append(dist.P2POp(dist.irecv, self.state.planes(0, d), p.rank - 1, self.group))
+            self.log.records.append(CommRecord(self.round, f"r{p.rank - 1}_to_r{p.rank}",
+                                               p.bytes_per_message))
+        if p.rank < p.world - 1:
+            ops.append(dist.P2POp(dist.isend, self.state.planes(p.ghost_lo + p.own - d, d),
+                                  p.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, self.state.planes(p.ghost_lo + p.own, d),
+                                  p.rank + 1, self.group))
+            self.log.records.append(CommRecord(self.round, f"r{p.rank + 1}_to_r{p.rank}",
+                                               p.bytes_per_message))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            for op in ops[::2]:
+                self.exchange_bytes += op.tensor.numel() * op.tensor.element_size()
+
+    def advance(self, n: int):
+        if n > self.fused_steps:
+            raise ValueError("a round advances at most k = depth / r steps")
+        if self.plan.world > 1:
+            self.exchange()
+        st = self.state.advance(n)
+        # ghost planes recomputed by this rank (HaloWorker::tally_ghost)
+        cross = 1
+        for e in self.plan.global_extent[1:]:
+            cross *= e
+        self.log.ghost_recompute_points += (self.plan.ghost_lo + self.plan.ghost_hi) * cross * n
+        self.round += 1
+        return st
+
+    def run(self, steps: int):
+        """ceil(T/k) rounds (scheduler.cpp:471-474)."""
+        left = int(steps)
+        while left > 0:
+            n = min(self.fused_steps, left)
+            self.advance(n)
+            left -= n
+
+    def own_rows(self):
+        """Owned rows of the local read buffer as a padded-shape ndarray
+        (host state only)."""
+        g = self.state.g
+        h0 = g.halo[0]
+        return g.padded(g.parity)[h0 + self.plan.ghost_lo:h0 + self.plan.ghost_lo + self.plan.own]
+
+    def comm_summary(self) -> dict:
+        return {"rounds": self.round, "messages_sent": len(self.log.records),
+                "bytes_per_message": self.plan.bytes_per_message,
+                "halo_depth": self.plan.depth, "fused_steps": self.fused_steps,
+                "bytes_sent": self.exchange_bytes,
+                "ghost_recompute_points": self.log.ghost_recompute_points}
