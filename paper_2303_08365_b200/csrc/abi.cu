@@ -6,6 +6,7 @@
 #include <array>
 #include <functional>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -18,6 +19,7 @@ namespace tsr {
 
 extern const Engine kStar3dR1Engine;
 extern const Engine kStream2dEngine;
+extern const Engine kTb3dEngine;
 
 namespace {
 
@@ -150,10 +152,15 @@ Status check_layout(const Geo& g, const tsr_layout* l) {
     return Status::Ok();
 }
 
+// Tuned engines in preference order.  TSR_ENGINE=<name> (environment) pins
+// one by name for A/B measurements; it never falls back to the CPU.
 const Engine* find_engine(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
-    static const Engine* const engines[] = {&kStar3dR1Engine, &kStream2dEngine};
-    for (const Engine* e : engines)
+    static const Engine* const engines[] = {&kTb3dEngine, &kStar3dR1Engine, &kStream2dEngine};
+    const char* pin = std::getenv("TSR_ENGINE");
+    for (const Engine* e : engines) {
+        if (pin && *pin && std::strcmp(pin, e->name) != 0) continue;
         if (e->supports(g, t, max_fused, default_fused)) return e;
+    }
     return nullptr;
 }
 

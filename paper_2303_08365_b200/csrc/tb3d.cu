@@ -1,0 +1,416 @@
+// tb3d.cu — 3-D radius-1 star (7-point) sweep with K time steps fused per
+// HBM pass: the paper's three tiers rebuilt for sm_100a.
+//
+//  * Memory tier: each CTA owns an output tile of (32-2(K-1)) x (64-2(K-1))
+//    cells of the (a1, a2) plane and streams a chunk of a0 planes.  Level-0
+//    planes (the tile plus a (K-1)+1 halo ring) arrive by TMA
+//    (cp.async.bulk.tensor.3d) into a 4-stage shared-memory ring guarded by
+//    mbarriers, three planes ahead of use.
+//  * SMEM tier (locality enhancer): levels 1..K-1 are computed on shrinking
+//    regions (overlapped tiling, the halo shrinks by one cell per level) as
+//    a wavefront along a0 — level l works on plane t-l while plane t
+//    arrives — so K steps cost one HBM read and one HBM write per cell.
+//    Each level's newest plane sits in a double-buffered SMEM plane for the
+//    a1-neighbours of other warps; one __syncthreads per plane serves all K
+//    levels.
+//  * Register tier (pattern mapping): a thread owns a 4 (a1) x 2 (a2) stack
+//    of columns and keeps, per level, the previous and current plane in
+//    registers (the a0-neighbours); a2-neighbours come from the adjacent lane
+//    by warp shuffle, a1-neighbours inside the stack from its own registers.
+//
+// Per point and level the arithmetic is apply_box's
+// (proj/include/tessera/naive.hpp:69-82): acc = 0, then the seven taps in
+// canonical order (-1,0,0) (0,-1,0) (0,0,-1) (0,0,0) (0,0,1) (0,1,0) (1,0,0).
+// Cells outside the interior keep their level-0 value at every level
+// (Dirichlet halo, grid.hpp:14-18), so EXACT mode is bitwise naive_run.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace tsr {
+
+namespace {
+
+constexpr int R1X = 64;  // level-1 region width  (a2)
+constexpr int R1Y = 32;  // level-1 region height (a1)
+constexpr int VX = 2;    // columns per thread along a2
+constexpr int VY = 4;    // columns per thread along a1
+constexpr int NLX = R1X / VX;  // 32 lanes
+constexpr int NLY = R1Y / VY;  // 8 warps
+constexpr int NT = NLX * NLY;  // 256 threads
+constexpr int BX0 = R1X + 4;   // TMA box width: 2 extra columns per side (16-B aligned rows)
+constexpr int BY0 = R1Y + 2;   // TMA box height: 1 extra row per side
+constexpr int STAGES = 4;
+constexpr int LEVY = R1Y + 2;  // level buffer rows (1 padding row per side)
+
+template <typename T>
+struct Pair;
+template <>
+struct Pair<double> {
+    using type = double2;
+};
+template <>
+struct Pair<float> {
+    using type = float2;
+};
+
+template <typename T>
+constexpr int slot_bytes() {
+    return (BX0 * BY0 * (int)sizeof(T) + 1023) / 1024 * 1024;
+}
+template <typename T>
+constexpr int lev_bytes() {
+    return (LEVY * R1X * (int)sizeof(T) + 127) / 128 * 128;
+}
+template <typename T, int K>
+constexpr int smem_bytes() {
+    return STAGES * slot_bytes<T>() + 2 * (K - 1) * lev_bytes<T>() + STAGES * 8;
+}
+
+template <typename T>
+struct TbArgs {
+    int n0, n1, n2;
+    int tiles_x, tiles_y;
+    int chunk;
+    int h0, h1, off2;
+    long long pitch0, pitch1, origin;
+    T w[7];
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned addr = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_plane(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+        "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+template <bool EXACT, typename T>
+__device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T right, T down,
+                                      T next) {
+    T acc = first<EXACT>(w[0], prev);
+    acc = madd<EXACT>(acc, w[1], up);
+    acc = madd<EXACT>(acc, w[2], left);
+    acc = madd<EXACT>(acc, w[3], c);
+    acc = madd<EXACT>(acc, w[4], right);
+    acc = madd<EXACT>(acc, w[5], down);
+    return madd<EXACT>(acc, w[6], next);
+}
+
+template <typename T, int K, bool EXACT>
+__global__ void __launch_bounds__(NT, 1)
+    tb3d_kernel(T* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
+                const __grid_constant__ TbArgs<T> a) {
+    using P2 = typename Pair<T>::type;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
+    constexpr int LEV = lev_bytes<T>() / (int)sizeof(T);
+    T* ring = reinterpret_cast<T*>(smem);
+    T* lev = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T>());
+    uint64_t* bar =
+        reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>() + 2 * (K - 1) * lev_bytes<T>());
+
+    const int tid = threadIdx.x;
+    const int lx = tid & 31, ly = tid >> 5;
+    const int tile = blockIdx.x;
+    const int bx = tile % a.tiles_x;
+    const int by = (tile / a.tiles_x) % a.tiles_y;
+    const int bz = tile / (a.tiles_x * a.tiles_y);
+    constexpr int TX = R1X - 2 * (K - 1), TY = R1Y - 2 * (K - 1);
+    const int gx = bx * TX - (K - 1);  // global a2 of region-1 column 0
+    const int gy = by * TY - (K - 1);  // global a1 of region-1 row 0
+    const int i0 = bz * a.chunk;
+    const int i1 = min(i0 + a.chunk, a.n0);
+    const int t_begin = i0 - K, t_end = i1 + K;
+    const int niter = t_end - t_begin;
+
+    // Columns owned: region-1 (y, x) = (VY*ly + cy, VX*lx + cx).
+    const int x = VX * lx, y = VY * ly;
+    bool cint[VY][VX], cout[VY][VX];
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) {
+            const int ga1 = gy + y + cy, ga2 = gx + x + cx;
+            cint[cy][cx] = ga1 >= 0 && ga1 < a.n1 && ga2 >= 0 && ga2 < a.n2;
+            cout[cy][cx] = cint[cy][cx] && y + cy >= K - 1 && y + cy < R1Y - (K - 1) &&
+                           x + cx >= K - 1 && x + cx < R1X - (K - 1);
+        }
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap))
+                     : "memory");
+    }
+    __syncthreads();
+    constexpr unsigned kBoxBytes = BX0 * BY0 * sizeof(T);
+    const int c0 = a.off2 + gx - 2, c1 = a.h1 + gy - 1;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES && s < niter; ++s) {
+            mbar_expect_tx(&bar[s], kBoxBytes);
+            tma_load_plane(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + s);
+        }
+    }
+
+    T w[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) w[q] = a.w[q];
+
+    // History per level l = 0..K-1: H[l][0] = plane q-1, H[l][1] = plane q,
+    // q being the newest plane level l has produced.
+    T H[K][2][VY][VX];
+#pragma unroll
+    for (int l = 0; l < K; ++l)
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) H[l][s][cy][cx] = T(0);
+
+    for (int it = 0; it < niter; ++it) {
+        const int t = t_begin + it;
+        const int slot = it % STAGES;
+        mbar_wait(&bar[slot], (it / STAGES) & 1);
+        const T* P0 = ring + slot * SLOT;                         // level 0, plane t
+        const T* Pm = ring + ((it + STAGES - 1) % STAGES) * SLOT;  // level 0, plane t-1
+
+        // NL: the newest plane of level l-1 (plane t-l+1); level 0's is plane t.
+        T NL[VY][VX];
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy) {
+            const P2 v = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX0 + x + 2);
+            NL[cy][0] = v.x;
+            NL[cy][1] = v.y;
+        }
+
+#pragma unroll
+        for (int l = 1; l <= K; ++l) {
+            const int p = t - l;  // plane produced by level l in this iteration
+            const bool pint = p >= 0 && p < a.n0;
+            // Rows y-1 and y+VY of level l-1 at plane p (other warps' stacks).
+            P2 u, d;
+            if (l == 1) {
+                u = *reinterpret_cast<const P2*>(Pm + (y) * BX0 + x + 2);
+                d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX0 + x + 2);
+            } else {
+                const T* L = lev + ((l - 2) * 2 + (p & 1)) * LEV;
+                u = *reinterpret_cast<const P2*>(L + (y) * R1X + x);
+                d = *reinterpret_cast<const P2*>(L + (y + VY + 1) * R1X + x);
+            }
+            T res[VY][VX];
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy) {
+                const T c0v = H[l - 1][1][cy][0], c1v = H[l - 1][1][cy][1];
+                T left = __shfl_up_sync(0xffffffffu, c1v, 1);
+                T right = __shfl_down_sync(0xffffffffu, c0v, 1);
+                if (l == 1) {  // region-1 edge columns read the level-0 halo ring
+                    if (lx == 0) left = Pm[(y + cy + 1) * BX0 + 1];
+                    if (lx == NLX - 1) right = Pm[(y + cy + 1) * BX0 + R1X + 2];
+                }
+                const T up0 = cy == 0 ? u.x : H[l - 1][1][cy - 1][0];
+                const T up1 = cy == 0 ? u.y : H[l - 1][1][cy - 1][1];
+                const T dn0 = cy == VY - 1 ? d.x : H[l - 1][1][cy + 1][0];
+                const T dn1 = cy == VY - 1 ? d.y : H[l - 1][1][cy + 1][1];
+                const T s0 = stencil7<EXACT>(w, H[l - 1][0][cy][0], up0, left, c0v, c1v, dn0,
+                                             NL[cy][0]);
+                const T s1 = stencil7<EXACT>(w, H[l - 1][0][cy][1], up1, c0v, c1v, right, dn1,
+                                             NL[cy][1]);
+                res[cy][0] = (pint && cint[cy][0]) ? s0 : c0v;
+                res[cy][1] = (pint && cint[cy][1]) ? s1 : c1v;
+            }
+            // Level l-1 history advances to planes (p, p+1).
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) {
+                    H[l - 1][0][cy][cx] = H[l - 1][1][cy][cx];
+                    H[l - 1][1][cy][cx] = NL[cy][cx];
+                }
+            if (l < K) {
+                // Publish the stack's top and bottom rows for the warps above/below.
+                T* L = lev + ((l - 1) * 2 + (p & 1)) * LEV;
+                P2 top, bot;
+                top.x = res[0][0], top.y = res[0][1];
+                bot.x = res[VY - 1][0], bot.y = res[VY - 1][1];
+                *reinterpret_cast<P2*>(L + (y + 1) * R1X + x) = top;
+                *reinterpret_cast<P2*>(L + (y + VY) * R1X + x) = bot;
+#pragma unroll
+                for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                    for (int cx = 0; cx < VX; ++cx) NL[cy][cx] = res[cy][cx];
+            } else if (p >= i0 && p < i1) {
+                T* o = out + a.origin + (long long)p * a.pitch0 + (long long)(gy + y) * a.pitch1 +
+                       (gx + x);
+#pragma unroll
+                for (int cy = 0; cy < VY; ++cy) {
+#pragma unroll
+                    for (int cx = 0; cx < VX; ++cx)
+                        if (cout[cy][cx]) o[cy * a.pitch1 + cx] = res[cy][cx];
+                }
+            }
+        }
+        __syncthreads();
+        // Plane t-1's slot is free: refill it with plane t-1+STAGES.
+        if (tid == 0 && it >= 1 && it - 1 + STAGES < niter) {
+            const int s = (it - 1) % STAGES;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[s], kBoxBytes);
+            tma_load_plane(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t + STAGES - 1);
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <typename T>
+Status make_map(const Geo& g, const void* base, CUtensorMap* m) {
+    auto enc = encode_fn();
+    if (!enc) return Status::Err(TSR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)g.pitch[1], (cuuint64_t)(g.n[1] + 2 * g.h[1]),
+                          (cuuint64_t)(g.n[0] + 2 * g.h[0])};
+    cuuint64_t strides[2] = {(cuuint64_t)(g.pitch[1] * sizeof(T)),
+                             (cuuint64_t)(g.pitch[0] * sizeof(T))};
+    cuuint32_t box[3] = {BX0, BY0, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return Status::Err(TSR_ECUDA, "cuTensorMapEncodeTiled failed");
+    return Status::Ok();
+}
+
+constexpr int kMaxK = 4;
+
+bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
+    if (t.dims != 3 || t.shape != TSR_STAR || t.radius != 1 || t.ntaps != 7) return false;
+    // 32-bit plane / row indices inside the kernel
+    if (g.n[0] + 2 * g.h[0] > (1 << 30) || g.n[1] + 2 * g.h[1] > (1 << 30)) return false;
+    *max_fused = kMaxK;
+    *default_fused = 3;
+    return true;
+}
+
+template <typename T, int K, bool EXACT>
+Status launch_k(const LaunchCtx& c, const void* in, void* out) {
+    const Geo& g = *c.g;
+    CUtensorMap map;
+    Status s = make_map<T>(g, in, &map);
+    if (!s.ok()) return s;
+    TbArgs<T> a;
+    a.n0 = (int)g.n[0];
+    a.n1 = (int)g.n[1];
+    a.n2 = (int)g.n[2];
+    constexpr int TX = R1X - 2 * (K - 1), TY = R1Y - 2 * (K - 1);
+    a.tiles_x = (int)((g.n[2] + TX - 1) / TX);
+    a.tiles_y = (int)((g.n[1] + TY - 1) / TY);
+    const long long tiles = (long long)a.tiles_x * a.tiles_y;
+    // Chunk a0 so the CTA count fills whole waves of 148 SMs (1 CTA/SM for
+    // K >= 3, 2 for K <= 2) with chunks of at least 48 planes.
+    const int per_sm = smem_bytes<T, K>() * 2 <= 227 * 1024 ? 2 : 1;
+    const long long slots = 148LL * per_sm;
+    int best_chunk = (int)g.n[0];
+    double best = 1e30;
+    for (int nz = 1; nz <= 64; ++nz) {
+        const int chunk = (int)((g.n[0] + nz - 1) / nz);
+        if (chunk < 48 && nz > 1) break;
+        const long long ctas = tiles * ((g.n[0] + chunk - 1) / chunk);
+        const long long waves = (ctas + slots - 1) / slots;
+        // cost ~ waves * (chunk + 2K) planes
+        const double cost = (double)waves * (chunk + 2 * K);
+        if (cost < best) {
+            best = cost;
+            best_chunk = chunk;
+        }
+    }
+    a.chunk = best_chunk;
+    a.h0 = (int)g.h[0];
+    a.h1 = (int)g.h[1];
+    a.off2 = (int)g.off2;
+    a.pitch0 = g.pitch[0];
+    a.pitch1 = g.pitch[1];
+    a.origin = g.origin;
+    for (int q = 0; q < 7; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
+    const long long nchunks = (g.n[0] + a.chunk - 1) / a.chunk;
+    const unsigned grid = (unsigned)(tiles * nchunks);
+    constexpr int bytes = smem_bytes<T, K>();
+    static bool attr[64] = {};
+    int dev = 0;
+    TSR_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return Status::Err(TSR_EUNSUPPORTED, "device ordinal >= 64");
+    if (!attr[dev]) {
+        TSR_CUDA_TRY(cudaFuncSetAttribute(tb3d_kernel<T, K, EXACT>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        attr[dev] = true;
+    }
+    tb3d_kernel<T, K, EXACT><<<grid, NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);
+    TSR_CUDA_TRY(cudaGetLastError());
+    return Status::Ok();
+}
+
+template <typename T, bool EXACT>
+Status launch_m(const LaunchCtx& c, const void* in, void* out, int k) {
+    switch (k) {
+        case 1: return launch_k<T, 1, EXACT>(c, in, out);
+        case 2: return launch_k<T, 2, EXACT>(c, in, out);
+        case 3: return launch_k<T, 3, EXACT>(c, in, out);
+        case 4: return launch_k<T, 4, EXACT>(c, in, out);
+        default: return Status::Err(TSR_EUNSUPPORTED, "tb3d: fused steps must be 1..4");
+    }
+}
+
+Status run(const LaunchCtx& c, const void* in, void* out, int k) {
+    if (c.g->dtype == TSR_F64)
+        return c.exact ? launch_m<double, true>(c, in, out, k)
+                       : launch_m<double, false>(c, in, out, k);
+    return c.exact ? launch_m<float, true>(c, in, out, k) : launch_m<float, false>(c, in, out, k);
+}
+
+}  // namespace
+
+extern const Engine kTb3dEngine = {"star3d_r1_tb", supports, run};
+
+}  // namespace tsr

@@ -68,17 +68,34 @@ def test_fused_2d_bitwise_all_k(ts, orc, name, dt):
             assert halos_equal(a, b)
 
 
+@pytest.mark.parametrize("fused", [1, 2, 3, 4])
 @pytest.mark.parametrize("dt", ["f64", "f32"])
-def test_heat3d_tuned_bitwise(ts, orc, dt):
+def test_heat3d_tuned_bitwise(ts, orc, dt, fused):
+    """tb3d: every fused depth, tiles cut by the grid edge in a1/a2, chunked
+    a0, halo wider than r, grids smaller than one tile."""
     k = ts.find_benchmark("Heat-3D").kernel
-    for extent, halo, steps in [([17, 13, 35], [1, 1, 1], 5), ([40, 33, 70], [2, 1, 3], 4),
-                                ([3, 3, 3], [1, 1, 1], 3)]:
+    for extent, halo, steps in [([17, 13, 35], [1, 1, 1], 5), ([40, 33, 70], [2, 1, 3], 7),
+                                ([3, 3, 3], [1, 1, 1], 3), ([130, 70, 131], [1, 1, 1], 4)]:
         a = random_grid(ts, orc, extent, halo, sum(extent), dt)
         b = a.copy()
-        st = ts.run_gpu(a, k, steps, engine="tuned")
+        st = ts.run_gpu(a, k, steps, fused_steps=fused, engine="tuned")
         orc.naive_run(b, k, steps)
-        assert st.engine == "tuned"
+        assert st.engine == "tuned" and st.fused_steps == fused
         assert both_buffers_equal(a, b), (extent, steps)
+        assert halos_equal(a, b)
+
+
+def test_star7_general_weights_3d(ts, orc):
+    """Non-uniform, non-power-of-two 7-point weights (tap order matters)."""
+    w = [((-1, 0, 0), 0.11), ((0, -1, 0), 0.13), ((0, 0, -1), 0.17), ((0, 0, 0), 0.19),
+         ((0, 0, 1), 0.07), ((0, 1, 0), 0.2), ((1, 0, 0), 0.13)]
+    k = ts.make_kernel(3, "star", 1, w)
+    for fused in (1, 2, 3, 4):
+        a = random_grid(ts, orc, [37, 45, 80], [1, 1, 1], fused)
+        b = a.copy()
+        ts.run_gpu(a, k, 9, fused_steps=fused)
+        orc.naive_run(b, k, 9)
+        assert both_buffers_equal(a, b), fused
 
 
 @pytest.mark.parametrize("name", ["Heat-1D", "Star-1D5P", "Box-2D25P", "Box-3D27P"])
