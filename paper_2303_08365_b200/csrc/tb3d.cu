@@ -39,7 +39,6 @@ constexpr int VY = 4;    // columns per thread along a1
 constexpr int NLX = R1X / VX;  // 32 lanes
 constexpr int NLY = R1Y / VY;  // 8 warps
 constexpr int NT = NLX * NLY;  // 256 threads
-constexpr int BX0 = R1X + 4;   // TMA box width: 2 extra columns per side (16-B aligned rows)
 constexpr int BY0 = R1Y + 2;   // TMA box height: 1 extra row per side
 constexpr int STAGES = 4;
 constexpr int LEVY = R1Y + 2;  // level buffer rows (1 padding row per side)
@@ -55,9 +54,23 @@ struct Pair<float> {
     using type = float2;
 };
 
+// TMA boxes must start on a 16-byte boundary of the innermost dimension, so
+// the ring carries PADL = 16/sizeof(T) columns left of region-1 (and as many
+// right), and the region's left overlap Hx is rounded up to that vector.
+template <typename T>
+constexpr int VEC = 16 / (int)sizeof(T);
+template <typename T>
+constexpr int PADL = VEC<T>;
+template <typename T>
+constexpr int BX0 = R1X + 2 * PADL<T>;  // TMA box width
+template <typename T, int K>
+constexpr int HXL = (K - 1 + VEC<T> - 1) / VEC<T> * VEC<T>;  // left overlap
+template <typename T, int K>
+constexpr int TXO = (R1X - HXL<T, K> - (K - 1)) / VEC<T> * VEC<T>;  // output tile width
+
 template <typename T>
 constexpr int slot_bytes() {
-    return (BX0 * BY0 * (int)sizeof(T) + 1023) / 1024 * 1024;
+    return (BX0<T> * BY0 * (int)sizeof(T) + 1023) / 1024 * 1024;
 }
 template <typename T>
 constexpr int lev_bytes() {
@@ -145,8 +158,9 @@ __global__ void __launch_bounds__(NT, 1)
     const int bx = tile % a.tiles_x;
     const int by = (tile / a.tiles_x) % a.tiles_y;
     const int bz = tile / (a.tiles_x * a.tiles_y);
-    constexpr int TX = R1X - 2 * (K - 1), TY = R1Y - 2 * (K - 1);
-    const int gx = bx * TX - (K - 1);  // global a2 of region-1 column 0
+    constexpr int TX = TXO<T, K>, TY = R1Y - 2 * (K - 1);
+    constexpr int BX = BX0<T>, PL = PADL<T>, HX = HXL<T, K>;
+    const int gx = bx * TX - HX;       // global a2 of region-1 column 0
     const int gy = by * TY - (K - 1);  // global a1 of region-1 row 0
     const int i0 = bz * a.chunk;
     const int i1 = min(i0 + a.chunk, a.n0);
@@ -163,7 +177,7 @@ __global__ void __launch_bounds__(NT, 1)
             const int ga1 = gy + y + cy, ga2 = gx + x + cx;
             cint[cy][cx] = ga1 >= 0 && ga1 < a.n1 && ga2 >= 0 && ga2 < a.n2;
             cout[cy][cx] = cint[cy][cx] && y + cy >= K - 1 && y + cy < R1Y - (K - 1) &&
-                           x + cx >= K - 1 && x + cx < R1X - (K - 1);
+                           x + cx >= HX && x + cx < HX + TX;
         }
 
     if (tid == 0) {
@@ -173,8 +187,8 @@ __global__ void __launch_bounds__(NT, 1)
                      : "memory");
     }
     __syncthreads();
-    constexpr unsigned kBoxBytes = BX0 * BY0 * sizeof(T);
-    const int c0 = a.off2 + gx - 2, c1 = a.h1 + gy - 1;
+    constexpr unsigned kBoxBytes = BX * BY0 * sizeof(T);
+    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned
     if (tid == 0) {
         for (int s = 0; s < STAGES && s < niter; ++s) {
             mbar_expect_tx(&bar[s], kBoxBytes);
@@ -209,7 +223,7 @@ __global__ void __launch_bounds__(NT, 1)
         T NL[VY][VX];
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy) {
-            const P2 v = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX0 + x + 2);
+            const P2 v = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
             NL[cy][0] = v.x;
             NL[cy][1] = v.y;
         }
@@ -221,8 +235,8 @@ __global__ void __launch_bounds__(NT, 1)
             // Rows y-1 and y+VY of level l-1 at plane p (other warps' stacks).
             P2 u, d;
             if (l == 1) {
-                u = *reinterpret_cast<const P2*>(Pm + (y) * BX0 + x + 2);
-                d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX0 + x + 2);
+                u = *reinterpret_cast<const P2*>(Pm + (y) * BX + x + PL);
+                d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX + x + PL);
             } else {
                 const T* L = lev + ((l - 2) * 2 + (p & 1)) * LEV;
                 u = *reinterpret_cast<const P2*>(L + (y) * R1X + x);
@@ -235,8 +249,8 @@ __global__ void __launch_bounds__(NT, 1)
                 T left = __shfl_up_sync(0xffffffffu, c1v, 1);
                 T right = __shfl_down_sync(0xffffffffu, c0v, 1);
                 if (l == 1) {  // region-1 edge columns read the level-0 halo ring
-                    if (lx == 0) left = Pm[(y + cy + 1) * BX0 + 1];
-                    if (lx == NLX - 1) right = Pm[(y + cy + 1) * BX0 + R1X + 2];
+                    if (lx == 0) left = Pm[(y + cy + 1) * BX + PL - 1];
+                    if (lx == NLX - 1) right = Pm[(y + cy + 1) * BX + R1X + PL];
                 }
                 const T up0 = cy == 0 ? u.x : H[l - 1][1][cy - 1][0];
                 const T up1 = cy == 0 ? u.y : H[l - 1][1][cy - 1][1];
@@ -312,7 +326,7 @@ Status make_map(const Geo& g, const void* base, CUtensorMap* m) {
                           (cuuint64_t)(g.n[0] + 2 * g.h[0])};
     cuuint64_t strides[2] = {(cuuint64_t)(g.pitch[1] * sizeof(T)),
                              (cuuint64_t)(g.pitch[0] * sizeof(T))};
-    cuuint32_t box[3] = {BX0, BY0, 1};
+    cuuint32_t box[3] = {(cuuint32_t)BX0<T>, BY0, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
@@ -344,7 +358,7 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.n0 = (int)g.n[0];
     a.n1 = (int)g.n[1];
     a.n2 = (int)g.n[2];
-    constexpr int TX = R1X - 2 * (K - 1), TY = R1Y - 2 * (K - 1);
+    constexpr int TX = TXO<T, K>, TY = R1Y - 2 * (K - 1);
     a.tiles_x = (int)((g.n[2] + TX - 1) / TX);
     a.tiles_y = (int)((g.n[1] + TY - 1) / TY);
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
