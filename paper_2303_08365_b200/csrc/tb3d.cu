@@ -13,7 +13,7 @@
 //    Each level's newest plane sits in a double-buffered SMEM plane for the
 //    a1-neighbours of other warps; one __syncthreads per plane serves all K
 //    levels.
-//  * Register tier (pattern mapping): a thread owns a 4 (a1) x 2 (a2) stack
+//  * Register tier (pattern mapping): a thread owns a 2 (a1) x 2 (a2) stack
 //    of columns and keeps, per level, the previous and current plane in
 //    registers (the a0-neighbours); a2-neighbours come from the adjacent lane
 //    by warp shuffle, a1-neighbours inside the stack from its own registers.
@@ -35,10 +35,10 @@ namespace {
 constexpr int R1X = 64;  // level-1 region width  (a2)
 constexpr int R1Y = 32;  // level-1 region height (a1)
 constexpr int VX = 2;    // columns per thread along a2
-constexpr int VY = 4;    // columns per thread along a1
+constexpr int VY = 2;    // columns per thread along a1
 constexpr int NLX = R1X / VX;  // 32 lanes
-constexpr int NLY = R1Y / VY;  // 8 warps
-constexpr int NT = NLX * NLY;  // 256 threads
+constexpr int NLY = R1Y / VY;  // 16 warps
+constexpr int NT = NLX * NLY;  // 512 threads
 constexpr int BY0 = R1Y + 2;   // TMA box height: 1 extra row per side
 constexpr int STAGES = 4;
 constexpr int LEVY = R1Y + 2;  // level buffer rows (1 padding row per side)
@@ -139,14 +139,108 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
     return madd<EXACT>(acc, w[6], next);
 }
 
+// One plane step of the wavefront (iteration `it`, PH = it % 3).  Register
+// history per level l: Hs[l][s] holds the level-l value of plane q with
+// (q - t_begin) % 3 == s, so the three-plane window rotates by renaming and
+// the time loop (unrolled by 3) needs no register moves.
+template <typename T, int K, bool EXACT, int PH>
+__device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
+                                          uint64_t* bar, int it, int t_begin, int i0, int i1,
+                                          int lx, int x, int y, int gx, int gy, bool tile_int,
+                                          const bool (&cint)[VY][VX], const bool (&cout)[VY][VX],
+                                          T (&Hs)[K][3][VY][VX]) {
+    using P2 = typename Pair<T>::type;
+    constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
+    constexpr int LEV = lev_bytes<T>() / (int)sizeof(T);
+    constexpr int BX = BX0<T>, PL = PADL<T>;
+    const int t = t_begin + it;
+    const int slot = it % STAGES;
+    mbar_wait(&bar[slot], (it / STAGES) & 1);
+    const T* P0 = ring + slot * SLOT;                         // level 0, plane t
+    const T* Pm = ring + ((it + STAGES - 1) % STAGES) * SLOT;  // level 0, plane t-1
+
+    // Level 0: plane t of the owned columns.
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy) {
+        const P2 v = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
+        Hs[0][PH][cy][0] = v.x;
+        Hs[0][PH][cy][1] = v.y;
+    }
+
+#pragma unroll
+    for (int l = 1; l <= K; ++l) {
+        const int p = t - l;  // plane level l produces now
+        const int sP = ((PH - l - 1) % 3 + 3) % 3;  // slot of plane p-1
+        const int sC = ((PH - l) % 3 + 3) % 3;      // slot of plane p
+        const int sN = ((PH - l + 1) % 3 + 3) % 3;  // slot of plane p+1
+        // a1-neighbour rows y-1 and y+VY of level l-1 at plane p.
+        P2 u, d;
+        if (l == 1) {
+            u = *reinterpret_cast<const P2*>(Pm + (y) * BX + x + PL);
+            d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX + x + PL);
+        } else {
+            const T* L = lev + ((l - 2) * 2 + (p & 1)) * LEV;
+            u = *reinterpret_cast<const P2*>(L + (y) * R1X + x);
+            d = *reinterpret_cast<const P2*>(L + (y + VY + 1) * R1X + x);
+        }
+        T res[VY][VX];
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy) {
+            const T c0v = Hs[l - 1][sC][cy][0], c1v = Hs[l - 1][sC][cy][1];
+            T left = __shfl_up_sync(0xffffffffu, c1v, 1);
+            T right = __shfl_down_sync(0xffffffffu, c0v, 1);
+            if (l == 1) {  // region-1 edge columns read the level-0 halo ring
+                if (lx == 0) left = Pm[(y + cy + 1) * BX + PL - 1];
+                if (lx == NLX - 1) right = Pm[(y + cy + 1) * BX + R1X + PL];
+            }
+            const T up0 = cy == 0 ? u.x : Hs[l - 1][sC][cy - 1][0];
+            const T up1 = cy == 0 ? u.y : Hs[l - 1][sC][cy - 1][1];
+            const T dn0 = cy == VY - 1 ? d.x : Hs[l - 1][sC][cy + 1][0];
+            const T dn1 = cy == VY - 1 ? d.y : Hs[l - 1][sC][cy + 1][1];
+            res[cy][0] = stencil7<EXACT>(a.w, Hs[l - 1][sP][cy][0], up0, left, c0v, c1v, dn0,
+                                         Hs[l - 1][sN][cy][0]);
+            res[cy][1] = stencil7<EXACT>(a.w, Hs[l - 1][sP][cy][1], up1, c0v, c1v, right, dn1,
+                                         Hs[l - 1][sN][cy][1]);
+        }
+        // Dirichlet: cells outside the interior keep their level-0 value
+        // (warp-uniform branch; interior tiles on interior planes skip it).
+        if (!(tile_int && p >= 0 && p < a.n0)) {
+            const bool pint = p >= 0 && p < a.n0;
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx)
+                    if (!(pint && cint[cy][cx])) res[cy][cx] = Hs[l - 1][sC][cy][cx];
+        }
+        if (l < K) {
+            T* L = lev + ((l - 1) * 2 + (p & 1)) * LEV;
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy) {
+                P2 v;
+                v.x = res[cy][0];
+                v.y = res[cy][1];
+                *reinterpret_cast<P2*>(L + (y + cy + 1) * R1X + x) = v;
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) Hs[l][sC][cy][cx] = res[cy][cx];
+            }
+        } else if (p >= i0 && p < i1) {
+            T* o = out + a.origin + (long long)p * a.pitch0 + (long long)(gy + y) * a.pitch1 +
+                   (gx + x);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx)
+                    if (cout[cy][cx]) o[cy * a.pitch1 + cx] = res[cy][cx];
+        }
+    }
+}
+
 template <typename T, int K, bool EXACT>
 __global__ void __launch_bounds__(NT, 1)
     tb3d_kernel(T* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
                 const __grid_constant__ TbArgs<T> a) {
-    using P2 = typename Pair<T>::type;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
-    constexpr int LEV = lev_bytes<T>() / (int)sizeof(T);
     T* ring = reinterpret_cast<T*>(smem);
     T* lev = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T>());
     uint64_t* bar =
@@ -159,13 +253,14 @@ __global__ void __launch_bounds__(NT, 1)
     const int by = (tile / a.tiles_x) % a.tiles_y;
     const int bz = tile / (a.tiles_x * a.tiles_y);
     constexpr int TX = TXO<T, K>, TY = R1Y - 2 * (K - 1);
-    constexpr int BX = BX0<T>, PL = PADL<T>, HX = HXL<T, K>;
+    constexpr int PL = PADL<T>, HX = HXL<T, K>;
     const int gx = bx * TX - HX;       // global a2 of region-1 column 0
     const int gy = by * TY - (K - 1);  // global a1 of region-1 row 0
     const int i0 = bz * a.chunk;
     const int i1 = min(i0 + a.chunk, a.n0);
     const int t_begin = i0 - K, t_end = i1 + K;
     const int niter = t_end - t_begin;
+    const bool tile_int = gy >= 0 && gy + R1Y <= a.n1 && gx >= 0 && gx + R1X <= a.n2;
 
     // Columns owned: region-1 (y, x) = (VY*ly + cy, VX*lx + cx).
     const int x = VX * lx, y = VY * ly;
@@ -187,8 +282,8 @@ __global__ void __launch_bounds__(NT, 1)
                      : "memory");
     }
     __syncthreads();
-    constexpr unsigned kBoxBytes = BX * BY0 * sizeof(T);
-    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned
+    constexpr unsigned kBoxBytes = BX0<T> * BY0 * sizeof(T);
+    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned box start
     if (tid == 0) {
         for (int s = 0; s < STAGES && s < niter; ++s) {
             mbar_expect_tx(&bar[s], kBoxBytes);
@@ -196,111 +291,40 @@ __global__ void __launch_bounds__(NT, 1)
         }
     }
 
-    T w[7];
-#pragma unroll
-    for (int q = 0; q < 7; ++q) w[q] = a.w[q];
-
-    // History per level l = 0..K-1: H[l][0] = plane q-1, H[l][1] = plane q,
-    // q being the newest plane level l has produced.
-    T H[K][2][VY][VX];
+    T Hs[K][3][VY][VX];
 #pragma unroll
     for (int l = 0; l < K; ++l)
 #pragma unroll
-        for (int s = 0; s < 2; ++s)
+        for (int s = 0; s < 3; ++s)
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-                for (int cx = 0; cx < VX; ++cx) H[l][s][cy][cx] = T(0);
+                for (int cx = 0; cx < VX; ++cx) Hs[l][s][cy][cx] = T(0);
 
-    for (int it = 0; it < niter; ++it) {
-        const int t = t_begin + it;
-        const int slot = it % STAGES;
-        mbar_wait(&bar[slot], (it / STAGES) & 1);
-        const T* P0 = ring + slot * SLOT;                         // level 0, plane t
-        const T* Pm = ring + ((it + STAGES - 1) % STAGES) * SLOT;  // level 0, plane t-1
-
-        // NL: the newest plane of level l-1 (plane t-l+1); level 0's is plane t.
-        T NL[VY][VX];
-#pragma unroll
-        for (int cy = 0; cy < VY; ++cy) {
-            const P2 v = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
-            NL[cy][0] = v.x;
-            NL[cy][1] = v.y;
-        }
-
-#pragma unroll
-        for (int l = 1; l <= K; ++l) {
-            const int p = t - l;  // plane produced by level l in this iteration
-            const bool pint = p >= 0 && p < a.n0;
-            // Rows y-1 and y+VY of level l-1 at plane p (other warps' stacks).
-            P2 u, d;
-            if (l == 1) {
-                u = *reinterpret_cast<const P2*>(Pm + (y) * BX + x + PL);
-                d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX + x + PL);
-            } else {
-                const T* L = lev + ((l - 2) * 2 + (p & 1)) * LEV;
-                u = *reinterpret_cast<const P2*>(L + (y) * R1X + x);
-                d = *reinterpret_cast<const P2*>(L + (y + VY + 1) * R1X + x);
-            }
-            T res[VY][VX];
-#pragma unroll
-            for (int cy = 0; cy < VY; ++cy) {
-                const T c0v = H[l - 1][1][cy][0], c1v = H[l - 1][1][cy][1];
-                T left = __shfl_up_sync(0xffffffffu, c1v, 1);
-                T right = __shfl_down_sync(0xffffffffu, c0v, 1);
-                if (l == 1) {  // region-1 edge columns read the level-0 halo ring
-                    if (lx == 0) left = Pm[(y + cy + 1) * BX + PL - 1];
-                    if (lx == NLX - 1) right = Pm[(y + cy + 1) * BX + R1X + PL];
-                }
-                const T up0 = cy == 0 ? u.x : H[l - 1][1][cy - 1][0];
-                const T up1 = cy == 0 ? u.y : H[l - 1][1][cy - 1][1];
-                const T dn0 = cy == VY - 1 ? d.x : H[l - 1][1][cy + 1][0];
-                const T dn1 = cy == VY - 1 ? d.y : H[l - 1][1][cy + 1][1];
-                const T s0 = stencil7<EXACT>(w, H[l - 1][0][cy][0], up0, left, c0v, c1v, dn0,
-                                             NL[cy][0]);
-                const T s1 = stencil7<EXACT>(w, H[l - 1][0][cy][1], up1, c0v, c1v, right, dn1,
-                                             NL[cy][1]);
-                res[cy][0] = (pint && cint[cy][0]) ? s0 : c0v;
-                res[cy][1] = (pint && cint[cy][1]) ? s1 : c1v;
-            }
-            // Level l-1 history advances to planes (p, p+1).
-#pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
-#pragma unroll
-                for (int cx = 0; cx < VX; ++cx) {
-                    H[l - 1][0][cy][cx] = H[l - 1][1][cy][cx];
-                    H[l - 1][1][cy][cx] = NL[cy][cx];
-                }
-            if (l < K) {
-                // Publish the stack's top and bottom rows for the warps above/below.
-                T* L = lev + ((l - 1) * 2 + (p & 1)) * LEV;
-                P2 top, bot;
-                top.x = res[0][0], top.y = res[0][1];
-                bot.x = res[VY - 1][0], bot.y = res[VY - 1][1];
-                *reinterpret_cast<P2*>(L + (y + 1) * R1X + x) = top;
-                *reinterpret_cast<P2*>(L + (y + VY) * R1X + x) = bot;
-#pragma unroll
-                for (int cy = 0; cy < VY; ++cy)
-#pragma unroll
-                    for (int cx = 0; cx < VX; ++cx) NL[cy][cx] = res[cy][cx];
-            } else if (p >= i0 && p < i1) {
-                T* o = out + a.origin + (long long)p * a.pitch0 + (long long)(gy + y) * a.pitch1 +
-                       (gx + x);
-#pragma unroll
-                for (int cy = 0; cy < VY; ++cy) {
-#pragma unroll
-                    for (int cx = 0; cx < VX; ++cx)
-                        if (cout[cy][cx]) o[cy * a.pitch1 + cx] = res[cy][cx];
-                }
-            }
-        }
+    auto after = [&](int it) {
         __syncthreads();
         // Plane t-1's slot is free: refill it with plane t-1+STAGES.
         if (tid == 0 && it >= 1 && it - 1 + STAGES < niter) {
             const int s = (it - 1) % STAGES;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&bar[s], kBoxBytes);
-            tma_load_plane(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t + STAGES - 1);
+            tma_load_plane(ring + s * SLOT, &tmap, &bar[s], c0, c1,
+                           a.h0 + t_begin + it - 1 + STAGES);
+        }
+    };
+    for (int it = 0; it < niter; it += 3) {
+        tb3d_step<T, K, EXACT, 0>(a, out, ring, lev, bar, it, t_begin, i0, i1, lx, x, y, gx, gy,
+                                  tile_int, cint, cout, Hs);
+        after(it);
+        if (it + 1 < niter) {
+            tb3d_step<T, K, EXACT, 1>(a, out, ring, lev, bar, it + 1, t_begin, i0, i1, lx, x, y,
+                                      gx, gy, tile_int, cint, cout, Hs);
+            after(it + 1);
+        }
+        if (it + 2 < niter) {
+            tb3d_step<T, K, EXACT, 2>(a, out, ring, lev, bar, it + 2, t_begin, i0, i1, lx, x, y,
+                                      gx, gy, tile_int, cint, cout, Hs);
+            after(it + 2);
         }
     }
 }
@@ -362,10 +386,23 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.tiles_x = (int)((g.n[2] + TX - 1) / TX);
     a.tiles_y = (int)((g.n[1] + TY - 1) / TY);
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
-    // Chunk a0 so the CTA count fills whole waves of 148 SMs (1 CTA/SM for
-    // K >= 3, 2 for K <= 2) with chunks of at least 48 planes.
-    const int per_sm = smem_bytes<T, K>() * 2 <= 227 * 1024 ? 2 : 1;
-    const long long slots = 148LL * per_sm;
+    // Chunk a0 so the CTA count fills whole waves of resident CTAs, with
+    // chunks of at least 48 planes (the 2K-plane wavefront fill is overhead).
+    constexpr int bytes = smem_bytes<T, K>();
+    static bool attr[64] = {};
+    int dev = 0;
+    TSR_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return Status::Err(TSR_EUNSUPPORTED, "device ordinal >= 64");
+    if (!attr[dev]) {
+        TSR_CUDA_TRY(cudaFuncSetAttribute(tb3d_kernel<T, K, EXACT>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        attr[dev] = true;
+    }
+    int per_sm = 1, nsm = 148;
+    TSR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tb3d_kernel<T, K, EXACT>,
+                                                               NT, bytes));
+    TSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const long long slots = (long long)nsm * std::max(per_sm, 1);
     int best_chunk = (int)g.n[0];
     double best = 1e30;
     for (int nz = 1; nz <= 64; ++nz) {
@@ -373,8 +410,7 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
         if (chunk < 48 && nz > 1) break;
         const long long ctas = tiles * ((g.n[0] + chunk - 1) / chunk);
         const long long waves = (ctas + slots - 1) / slots;
-        // cost ~ waves * (chunk + 2K) planes
-        const double cost = (double)waves * (chunk + 2 * K);
+        const double cost = (double)waves * (chunk + 2 * K);  // planes per SM slot
         if (cost < best) {
             best = cost;
             best_chunk = chunk;
@@ -390,16 +426,6 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     for (int q = 0; q < 7; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     const long long nchunks = (g.n[0] + a.chunk - 1) / a.chunk;
     const unsigned grid = (unsigned)(tiles * nchunks);
-    constexpr int bytes = smem_bytes<T, K>();
-    static bool attr[64] = {};
-    int dev = 0;
-    TSR_CUDA_TRY(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 64) return Status::Err(TSR_EUNSUPPORTED, "device ordinal >= 64");
-    if (!attr[dev]) {
-        TSR_CUDA_TRY(cudaFuncSetAttribute(tb3d_kernel<T, K, EXACT>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        attr[dev] = true;
-    }
     tb3d_kernel<T, K, EXACT><<<grid, NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
