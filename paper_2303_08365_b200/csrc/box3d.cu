@@ -1,0 +1,245 @@
+// box3d.cu — 3-D radius-1 box (27-point) sweep, 2.5-D streaming with
+// per-plane partial sums.
+//
+// The oracle sums the 27 taps in lexicographic (di, dj, dk) order
+// (proj/src/kernel.cpp:19-43, naive.hpp:76-78): all nine taps of plane p-1,
+// then plane p, then plane p+1.  So output plane p's accumulator can be
+// advanced plane by plane as a0 streams past: when plane q sits in shared
+// memory, every thread reads its (4+2) x (4+2) neighbourhood once and
+//   * finishes the accumulator of output q-1 (taps di=+1) and stores it,
+//   * continues output q (taps di=0),
+//   * starts output q+1 (taps di=-1),
+// each accumulator seeing its taps in exactly the oracle's order.  One plane
+// read serves three outputs: 2.25 shared-memory loads per output instead of
+// 27.  Planes arrive by TMA (cp.async.bulk.tensor.3d) into a 4-stage
+// mbarrier ring.  FAST mode is one FMA per tap; EXACT a separately rounded
+// multiply and add (bitwise naive_run).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace tsr {
+
+namespace {
+
+constexpr int OX = 64;  // output tile width  (a2)
+constexpr int OY = 32;  // output tile height (a1)
+constexpr int VX = 4;   // outputs per thread along a2
+constexpr int VY = 4;   // outputs per thread along a1
+constexpr int NLX = OX / VX;   // 16
+constexpr int NLY = OY / VY;   // 8
+constexpr int NT = NLX * NLY;  // 128 threads
+constexpr int STAGES = 4;
+constexpr int BY = OY + 2;
+
+template <typename T>
+constexpr int PAD = 16 / (int)sizeof(T);  // 16-B aligned box start / rows
+template <typename T>
+constexpr int BXW = OX + 2 * PAD<T>;
+template <typename T>
+constexpr int slot_bytes() {
+    return (BXW<T> * BY * (int)sizeof(T) + 127) / 128 * 128;
+}
+template <typename T>
+constexpr int smem_bytes() {
+    return STAGES * slot_bytes<T>() + STAGES * 8;
+}
+
+template <typename T>
+struct BoxArgs {
+    int n0, n1, n2;
+    int tiles_x, tiles_y, chunk;
+    int h0, h1, off2;
+    long long pitch0, pitch1, origin;
+    T w[27];
+};
+
+template <typename T, int V>
+struct VecT;
+template <>
+struct VecT<float, 4> {
+    using type = float4;
+};
+template <>
+struct VecT<double, 2> {
+    using type = double2;
+};
+
+// Nine taps of one plane offset applied to the neighbourhood nb (rows y-1..y+VY,
+// cols x-1..x+VX) for every output of the thread's 4x4 tile.
+template <bool EXACT, bool START, typename T>
+__device__ __forceinline__ void apply9(const T* __restrict__ w, const T (&nb)[VY + 2][VX + 2],
+                                       T (&acc)[VY][VX]) {
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) {
+            T s = acc[cy][cx];
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj)
+#pragma unroll
+                for (int dk = 0; dk < 3; ++dk) {
+                    const T v = nb[cy + dj][cx + dk];
+                    if (START && dj == 0 && dk == 0)
+                        s = first<EXACT>(w[0], v);
+                    else
+                        s = madd<EXACT>(s, w[dj * 3 + dk], v);
+                }
+            acc[cy][cx] = s;
+        }
+}
+
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(NT) box3d_kernel(T* __restrict__ out,
+                                                  const __grid_constant__ CUtensorMap tmap,
+                                                  const __grid_constant__ BoxArgs<T> a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
+    constexpr int BX = BXW<T>, PL = PAD<T>;
+    T* ring = reinterpret_cast<T*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>());
+
+    const int tid = threadIdx.x;
+    const int lx = tid % NLX, ly = tid / NLX;
+    const int tile = blockIdx.x;
+    const int bx = tile % a.tiles_x;
+    const int by = (tile / a.tiles_x) % a.tiles_y;
+    const int bz = tile / (a.tiles_x * a.tiles_y);
+    const int gx = bx * OX, gy = by * OY;  // interior coords of the tile origin
+    const int i0 = bz * a.chunk;
+    const int i1 = min(i0 + a.chunk, a.n0);
+    // planes i0-1 .. i1 feed outputs i0 .. i1-1
+    const int t_begin = i0 - 1, niter = i1 - i0 + 2;
+    const int x = VX * lx, y = VY * ly;
+
+    bool ok[VY][VX];
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx)
+            ok[cy][cx] = gy + y + cy < a.n1 && gx + x + cx < a.n2;
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&tmap);
+    }
+    __syncthreads();
+    constexpr unsigned kBoxBytes = BX * BY * sizeof(T);
+    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;
+    if (tid == 0)
+        for (int s = 0; s < STAGES && s < niter; ++s) {
+            mbar_expect_tx(&bar[s], kBoxBytes);
+            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + s);
+        }
+
+    T accA[VY][VX], accB[VY][VX];  // outputs q+1 (started) and q (in progress)
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) accA[cy][cx] = accB[cy][cx] = T(0);
+
+    using V4 = typename VecT<T, 16 / sizeof(T)>::type;
+    constexpr int NV = 16 / sizeof(T);
+    for (int it = 0; it < niter; ++it) {
+        const int q = t_begin + it;  // plane in shared memory
+        const int slot = it % STAGES;
+        mbar_wait(&bar[slot], (it / STAGES) & 1);
+        const T* P = ring + slot * SLOT;
+        T nb[VY + 2][VX + 2];
+#pragma unroll
+        for (int r = 0; r < VY + 2; ++r) {
+            const T* row = P + (y + r) * BX + PL + x;  // region col x <-> ring col x+PL
+            nb[r][0] = row[-1];
+#pragma unroll
+            for (int v = 0; v < VX; v += NV) {
+                const V4 vv = *reinterpret_cast<const V4*>(row + v);
+                const T* e = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+                for (int u = 0; u < NV; ++u) nb[r][1 + v + u] = e[u];
+            }
+            nb[r][VX + 1] = row[VX];
+        }
+        __syncthreads();  // every thread has its neighbourhood: slot may be refilled
+        if (tid == 0 && it + STAGES < niter) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[slot], kBoxBytes);
+            tma_load_3d(ring + slot * SLOT, &tmap, &bar[slot], c0, c1,
+                        a.h0 + t_begin + it + STAGES);
+        }
+        // finish output q-1 (di = +1 taps)
+        apply9<EXACT, false>(a.w + 18, nb, accB);
+        const int po = q - 1;
+        if (it >= 2 && po < i1) {
+            T* o = out + a.origin + (long long)po * a.pitch0 + (long long)(gy + y) * a.pitch1 +
+                   (gx + x);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx)
+                    if (ok[cy][cx]) o[cy * a.pitch1 + cx] = accB[cy][cx];
+        }
+        // output q continues (di = 0), output q+1 starts (di = -1)
+        apply9<EXACT, false>(a.w + 9, nb, accA);
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < VX; ++cx) accB[cy][cx] = accA[cy][cx];
+        apply9<EXACT, true>(a.w, nb, accA);
+    }
+}
+
+bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
+    if (t.dims != 3 || t.shape != TSR_BOX || t.radius != 1 || t.ntaps != 27) return false;
+    if (g.n[0] + 2 * g.h[0] > (1 << 30) || g.n[1] + 2 * g.h[1] > (1 << 30)) return false;
+    *max_fused = 1;
+    *default_fused = 1;
+    return true;
+}
+
+template <typename T, bool EXACT>
+Status launch(const LaunchCtx& c, const void* in, void* out) {
+    const Geo& g = *c.g;
+    CUtensorMap map;
+    Status s = make_tmap_3d<T>(g, in, BXW<T>, BY, &map);
+    if (!s.ok()) return s;
+    BoxArgs<T> a;
+    a.n0 = (int)g.n[0];
+    a.n1 = (int)g.n[1];
+    a.n2 = (int)g.n[2];
+    a.tiles_x = (int)((g.n[2] + OX - 1) / OX);
+    a.tiles_y = (int)((g.n[1] + OY - 1) / OY);
+    a.h0 = (int)g.h[0];
+    a.h1 = (int)g.h[1];
+    a.off2 = (int)g.off2;
+    a.pitch0 = g.pitch[0];
+    a.pitch1 = g.pitch[1];
+    a.origin = g.origin;
+    for (int q = 0; q < 27; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
+    constexpr int bytes = smem_bytes<T>();
+    int per_sm = 1, nsm = 148;
+    s = occupancy(box3d_kernel<T, EXACT>, NT, bytes, &per_sm, &nsm);
+    if (!s.ok()) return s;
+    const long long tiles = (long long)a.tiles_x * a.tiles_y;
+    a.chunk = pick_chunk(g.n[0], tiles, (long long)nsm * per_sm, 2, 32);
+    const long long nchunks = (g.n[0] + a.chunk - 1) / a.chunk;
+    box3d_kernel<T, EXACT><<<(unsigned)(tiles * nchunks), NT, bytes, c.stream>>>(
+        static_cast<T*>(out), map, a);
+    TSR_CUDA_TRY(cudaGetLastError());
+    return Status::Ok();
+}
+
+Status run(const LaunchCtx& c, const void* in, void* out, int k) {
+    if (k != 1) return Status::Err(TSR_EUNSUPPORTED, "box3d fuses one step per pass");
+    if (c.g->dtype == TSR_F64)
+        return c.exact ? launch<double, true>(c, in, out) : launch<double, false>(c, in, out);
+    return c.exact ? launch<float, true>(c, in, out) : launch<float, false>(c, in, out);
+}
+
+}  // namespace
+
+extern const Engine kBox3dEngine = {"box3d_r1_planesum", supports, run};
+
+}  // namespace tsr

@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace tsr {
 
@@ -90,42 +91,6 @@ struct TbArgs {
     long long pitch0, pitch1, origin;
     T w[7];
 };
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(bar)),
-                 "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    const unsigned addr = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(addr),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_plane(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                               int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
-        "r"((unsigned)__cvta_generic_to_shared(bar))
-        : "memory");
-}
 
 template <bool EXACT, typename T>
 __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T right, T down,
@@ -278,8 +243,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap))
-                     : "memory");
+        prefetch_tmap(&tmap);
     }
     __syncthreads();
     constexpr unsigned kBoxBytes = BX0<T> * BY0 * sizeof(T);
@@ -287,7 +251,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (tid == 0) {
         for (int s = 0; s < STAGES && s < niter; ++s) {
             mbar_expect_tx(&bar[s], kBoxBytes);
-            tma_load_plane(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + s);
+            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + s);
         }
     }
 
@@ -308,7 +272,7 @@ __global__ void __launch_bounds__(NT, 1)
             const int s = (it - 1) % STAGES;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&bar[s], kBoxBytes);
-            tma_load_plane(ring + s * SLOT, &tmap, &bar[s], c0, c1,
+            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1,
                            a.h0 + t_begin + it - 1 + STAGES);
         }
     };
@@ -329,38 +293,6 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-template <typename T>
-Status make_map(const Geo& g, const void* base, CUtensorMap* m) {
-    auto enc = encode_fn();
-    if (!enc) return Status::Err(TSR_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[3] = {(cuuint64_t)g.pitch[1], (cuuint64_t)(g.n[1] + 2 * g.h[1]),
-                          (cuuint64_t)(g.n[0] + 2 * g.h[0])};
-    cuuint64_t strides[2] = {(cuuint64_t)(g.pitch[1] * sizeof(T)),
-                             (cuuint64_t)(g.pitch[0] * sizeof(T))};
-    cuuint32_t box[3] = {(cuuint32_t)BX0<T>, BY0, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
-                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                     3, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return Status::Err(TSR_ECUDA, "cuTensorMapEncodeTiled failed");
-    return Status::Ok();
-}
-
 constexpr int kMaxK = 4;
 
 bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
@@ -376,7 +308,7 @@ template <typename T, int K, bool EXACT>
 Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     const Geo& g = *c.g;
     CUtensorMap map;
-    Status s = make_map<T>(g, in, &map);
+    Status s = make_tmap_3d<T>(g, in, BX0<T>, BY0, &map);
     if (!s.ok()) return s;
     TbArgs<T> a;
     a.n0 = (int)g.n[0];
@@ -386,36 +318,13 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.tiles_x = (int)((g.n[2] + TX - 1) / TX);
     a.tiles_y = (int)((g.n[1] + TY - 1) / TY);
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
-    // Chunk a0 so the CTA count fills whole waves of resident CTAs, with
-    // chunks of at least 48 planes (the 2K-plane wavefront fill is overhead).
     constexpr int bytes = smem_bytes<T, K>();
-    static bool attr[64] = {};
-    int dev = 0;
-    TSR_CUDA_TRY(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 64) return Status::Err(TSR_EUNSUPPORTED, "device ordinal >= 64");
-    if (!attr[dev]) {
-        TSR_CUDA_TRY(cudaFuncSetAttribute(tb3d_kernel<T, K, EXACT>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        attr[dev] = true;
-    }
     int per_sm = 1, nsm = 148;
-    TSR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tb3d_kernel<T, K, EXACT>,
-                                                               NT, bytes));
-    TSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const long long slots = (long long)nsm * std::max(per_sm, 1);
-    int best_chunk = (int)g.n[0];
-    double best = 1e30;
-    for (int nz = 1; nz <= 64; ++nz) {
-        const int chunk = (int)((g.n[0] + nz - 1) / nz);
-        if (chunk < 48 && nz > 1) break;
-        const long long ctas = tiles * ((g.n[0] + chunk - 1) / chunk);
-        const long long waves = (ctas + slots - 1) / slots;
-        const double cost = (double)waves * (chunk + 2 * K);  // planes per SM slot
-        if (cost < best) {
-            best = cost;
-            best_chunk = chunk;
-        }
-    }
+    s = occupancy(tb3d_kernel<T, K, EXACT>, NT, bytes, &per_sm, &nsm);
+    if (!s.ok()) return s;
+    // a0 chunks: whole waves of resident CTAs, >= 48 planes (the 2K-plane
+    // wavefront fill is overhead)
+    const int best_chunk = pick_chunk(g.n[0], tiles, (long long)nsm * per_sm, 2 * K, 48);
     a.chunk = best_chunk;
     a.h0 = (int)g.h[0];
     a.h1 = (int)g.h[1];

@@ -1,0 +1,36 @@
+// tma.cu — host helpers behind tma.cuh.
+#include "tma.cuh"
+
+namespace tsr {
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    }();
+    return fn;
+}
+
+int pick_chunk(int64_t n0, int64_t tiles, int64_t slots, int overlap, int min_chunk) {
+    int64_t best_chunk = n0;
+    double best = 1e300;
+    for (int64_t nz = 1; nz <= 256; ++nz) {
+        const int64_t chunk = (n0 + nz - 1) / nz;
+        if (chunk < min_chunk && nz > 1) break;
+        const int64_t ctas = tiles * ((n0 + chunk - 1) / chunk);
+        const int64_t waves = (ctas + slots - 1) / slots;
+        const double cost = (double)waves * (double)(chunk + overlap);
+        if (cost < best) {
+            best = cost;
+            best_chunk = chunk;
+        }
+    }
+    return (int)best_chunk;
+}
+
+}  // namespace tsr

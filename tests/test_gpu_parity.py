@@ -104,9 +104,26 @@ def test_generic_engine_bitwise(ts, orc, name):
     ext = {1: [301], 2: [37, 41], 3: [11, 19, 23]}[k.dims]
     a = random_grid(ts, orc, ext, [k.radius] * k.dims, 5)
     b = a.copy()
-    ts.naive_run(a, k, 6)
+    st = ts.run_gpu(a, k, 6, engine="generic")
     orc.naive_run(b, k, 6)
+    assert st.engine == "generic"
     assert both_buffers_equal(a, b)
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_box27_planesum_bitwise(ts, orc, dt):
+    """box3d engine: per-plane partial sums keep the oracle's tap order;
+    tiles cut by the grid edge, chunked a0, halo wider than r."""
+    k = ts.find_benchmark("Box-3D27P").kernel
+    for extent, halo, steps in [([11, 19, 23], [1, 1, 1], 4), ([70, 45, 150], [2, 1, 3], 3),
+                                ([3, 3, 3], [1, 1, 1], 2)]:
+        a = random_grid(ts, orc, extent, halo, sum(extent), dt)
+        b = a.copy()
+        st = ts.run_gpu(a, k, steps, engine="tuned")
+        orc.naive_run(b, k, steps)
+        assert st.engine == "tuned"
+        assert both_buffers_equal(a, b), extent
+        assert halos_equal(a, b)
 
 
 @pytest.mark.parametrize("name", ["Heat-2D", "Box-2D9P", "Heat-3D", "Box-3D27P"])
