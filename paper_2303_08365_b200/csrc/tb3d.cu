@@ -92,10 +92,19 @@ struct TbArgs {
     T w[7];
 };
 
+// The reference starts every sum from +0 (naive.hpp:75); that accumulator can
+// never become -0, so dropping the leading "0 +" changes at most the sign of
+// a zero result, in intermediate levels too (x + (-0) == x + (+0) unless both
+// are zero).  tb3d_step restores the reference's +0 with one `+ 0.0` per
+// stored value instead of one per level and point.
 template <bool EXACT, typename T>
 __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T right, T down,
                                       T next) {
-    T acc = first<EXACT>(w[0], prev);
+    T acc;
+    if constexpr (EXACT)
+        acc = sizeof(T) == 8 ? (T)__dmul_rn((double)w[0], (double)prev) : (T)__fmul_rn((float)w[0], (float)prev);
+    else
+        acc = first<EXACT>(w[0], prev);
     acc = madd<EXACT>(acc, w[1], up);
     acc = madd<EXACT>(acc, w[2], left);
     acc = madd<EXACT>(acc, w[3], c);
@@ -108,7 +117,7 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 // history per level l: Hs[l][s] holds the level-l value of plane q with
 // (q - t_begin) % 3 == s, so the three-plane window rotates by renaming and
 // the time loop (unrolled by 3) needs no register moves.
-template <typename T, int K, bool EXACT, int PH>
+template <typename T, int K, bool EXACT, int PH, bool SEL>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
                                           uint64_t* bar, int it, int t_begin, int i0, int i1,
                                           int lx, int x, int y, int gx, int gy, bool tile_int,
@@ -168,8 +177,8 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                                          Hs[l - 1][sN][cy][1]);
         }
         // Dirichlet: cells outside the interior keep their level-0 value
-        // (warp-uniform branch; interior tiles on interior planes skip it).
-        if (!(tile_int && p >= 0 && p < a.n0)) {
+        // (only the SEL instantiation, used for edge tiles / edge planes).
+        if constexpr (SEL) {
             const bool pint = p >= 0 && p < a.n0;
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy)
@@ -195,7 +204,8 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
             for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx)
-                    if (cout[cy][cx]) o[cy * a.pitch1 + cx] = res[cy][cx];
+                    if (cout[cy][cx])
+                        o[cy * a.pitch1 + cx] = EXACT ? res[cy][cx] + T(0) : res[cy][cx];
         }
     }
 }
@@ -276,21 +286,30 @@ __global__ void __launch_bounds__(NT, 1)
                            a.h0 + t_begin + it - 1 + STAGES);
         }
     };
+    // Planes t-K..t-1 all interior and the tile clear of the a1/a2 boundary:
+    // no Dirichlet selects needed in this step (warp-uniform).
+    auto clear = [&](int it) {
+        const int t = t_begin + it;
+        return tile_int && t - K >= 0 && t - 1 < a.n0;
+    };
+#define TB3D_STEP(PH, IT)                                                                    \
+    if (clear(IT))                                                                           \
+        tb3d_step<T, K, EXACT, PH, false>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x, \
+                                          y, gx, gy, tile_int, cint, cout, Hs);              \
+    else                                                                                     \
+        tb3d_step<T, K, EXACT, PH, true>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x,  \
+                                         y, gx, gy, tile_int, cint, cout, Hs);               \
+    after(IT);
     for (int it = 0; it < niter; it += 3) {
-        tb3d_step<T, K, EXACT, 0>(a, out, ring, lev, bar, it, t_begin, i0, i1, lx, x, y, gx, gy,
-                                  tile_int, cint, cout, Hs);
-        after(it);
+        TB3D_STEP(0, it)
         if (it + 1 < niter) {
-            tb3d_step<T, K, EXACT, 1>(a, out, ring, lev, bar, it + 1, t_begin, i0, i1, lx, x, y,
-                                      gx, gy, tile_int, cint, cout, Hs);
-            after(it + 1);
+            TB3D_STEP(1, it + 1)
         }
         if (it + 2 < niter) {
-            tb3d_step<T, K, EXACT, 2>(a, out, ring, lev, bar, it + 2, t_begin, i0, i1, lx, x, y,
-                                      gx, gy, tile_int, cint, cout, Hs);
-            after(it + 2);
+            TB3D_STEP(2, it + 2)
         }
     }
+#undef TB3D_STEP
 }
 
 constexpr int kMaxK = 4;
