@@ -127,15 +127,20 @@ def fused_groups(steps: int, k: int) -> list[int]:
     return out
 
 
-def ncu_traffic(cfg_name: str):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    capture summary (profiles/), or None."""
+def ncu_traffic(cfg_name: str, kfused: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from the committed ncu launch list of this bench command
+    (profiles/ncu_traffic.json, written by tools/launch_summary.py), or None
+    when the committed capture is for another fused depth."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(cfg_name)
+            d = json.load(f).get(cfg_name)
+        if d and (f", {kfused}, " in d["kernel"]):
+            return d
     except Exception:
-        return None
+        pass
+    return None
 
 
 def cpu_baseline(ts, cfg, cfg_name, steps_cap=None):
@@ -301,7 +306,7 @@ def main():
     # the k steps the launch advances ("HBM-equivalent" for k > 1).
     alg_bytes = 2 * esize * points_per_gpu * kfused
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(args.config, kfused)
 
     e2e = None
     cpu = None
@@ -349,7 +354,9 @@ def main():
                           " exceed the 126 MB L2")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic,
+                     "traffic": traffic["bytes_per_launch"] if traffic else None,
+                     "traffic_source": (f"ncu launch list profiles/r01/{traffic['source']} "
+                                        f"({traffic['kernel']})") if traffic else None,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                      if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
                      "basis": (f"algorithmic {2 * esize} B per stencil update x {kfused} fused "
