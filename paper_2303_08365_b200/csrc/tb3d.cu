@@ -5,17 +5,14 @@
 //    cells of the (a1, a2) plane and streams a chunk of a0 planes.  Level-0
 //    planes (the tile plus a (K-1)+1 halo ring) arrive by TMA
 //    (cp.async.bulk.tensor.3d) into a 4-stage shared-memory ring guarded by
-//    mbarriers.
+//    mbarriers, three planes ahead of use.
 //  * SMEM tier (locality enhancer): levels 1..K-1 are computed on shrinking
 //    regions (overlapped tiling, the halo shrinks by one cell per level) as
 //    a wavefront along a0 — level l works on plane t-l while plane t
 //    arrives — so K steps cost one HBM read and one HBM write per cell.
-//    Each level's newest plane goes to a 3-deep SMEM plane buffer for the
-//    a1-neighbours of other warps.  There is no CTA-wide barrier in the loop:
-//    each warp publishes its progress (st.release) and waits only for its two
-//    a1-neighbour warps (ld.acquire), so warps drift and the FP64 pipe sees a
-//    smooth instruction stream; a dedicated producer warp refills a ring
-//    slot once every warp is past it.
+//    Each level's newest plane sits in a double-buffered SMEM plane for the
+//    a1-neighbours of other warps; one __syncthreads per plane serves all K
+//    levels.
 //  * Register tier (pattern mapping): a thread owns a 2 (a1) x 2 (a2) stack
 //    of columns and keeps, per level, the previous and current plane in
 //    registers (the a0-neighbours); a2-neighbours come from the adjacent lane
@@ -80,30 +77,9 @@ template <typename T>
 constexpr int lev_bytes() {
     return (LEVY * R1X * (int)sizeof(T) + 127) / 128 * 128;
 }
-constexpr int NLEV = 3;  // level-buffer depth: lets neighbouring warps drift by one plane
 template <typename T, int K>
 constexpr int smem_bytes() {
-    return STAGES * slot_bytes<T>() + NLEV * (K - 1) * lev_bytes<T>() + STAGES * 8 + NLY * 4;
-}
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];"
-                 : "=r"(v)
-                 : "r"((unsigned)__cvta_generic_to_shared(p))
-                 : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(p)),
-                 "r"(v)
-                 : "memory");
-}
-
-__device__ __forceinline__ void wait_progress(const int* p, int want) {
-    while (ld_acquire(p) < want) __nanosleep(20);
+    return STAGES * slot_bytes<T>() + 2 * (K - 1) * lev_bytes<T>() + STAGES * 8;
 }
 
 template <typename T>
@@ -143,8 +119,7 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 // the time loop (unrolled by 3) needs no register moves.
 template <typename T, int K, bool EXACT, int PH, bool SEL>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
-                                          uint64_t* bar, int it, int t_begin, int tb3, int i0,
-                                          int i1,
+                                          uint64_t* bar, int it, int t_begin, int i0, int i1,
                                           int lx, int x, int y, int gx, int gy, bool tile_int,
                                           const bool (&cint)[VY][VX], const bool (&cout)[VY][VX],
                                           T (&Hs)[K][3][VY][VX]) {
@@ -178,7 +153,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
             u = *reinterpret_cast<const P2*>(Pm + (y) * BX + x + PL);
             d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX + x + PL);
         } else {
-            const T* L = lev + ((l - 2) * NLEV + (tb3 + PH - l + 3 * K) % 3) * LEV;
+            const T* L = lev + ((l - 2) * 2 + (p & 1)) * LEV;
             u = *reinterpret_cast<const P2*>(L + (y) * R1X + x);
             d = *reinterpret_cast<const P2*>(L + (y + VY + 1) * R1X + x);
         }
@@ -212,7 +187,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                     if (!(pint && cint[cy][cx])) res[cy][cx] = Hs[l - 1][sC][cy][cx];
         }
         if (l < K) {
-            T* L = lev + ((l - 1) * NLEV + (tb3 + PH - l + 3 * K) % 3) * LEV;
+            T* L = lev + ((l - 1) * 2 + (p & 1)) * LEV;
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy) {
                 P2 v;
@@ -243,9 +218,8 @@ __global__ void __launch_bounds__(NT, 1)
     constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
     T* ring = reinterpret_cast<T*>(smem);
     T* lev = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T>());
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>() +
-                                                NLEV * (K - 1) * lev_bytes<T>());
-    int* prog = reinterpret_cast<int*>(bar + STAGES);  // planes finished, per compute warp
+    uint64_t* bar =
+        reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>() + 2 * (K - 1) * lev_bytes<T>());
 
     const int tid = threadIdx.x;
     const int lx = tid & 31, ly = tid >> 5;
@@ -261,18 +235,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int i1 = min(i0 + a.chunk, a.n0);
     const int t_begin = i0 - K, t_end = i1 + K;
     const int niter = t_end - t_begin;
-    const int tb3 = ((t_begin % 3) + 3) % 3;
     const bool tile_int = gy >= 0 && gy + R1Y <= a.n1 && gx >= 0 && gx + R1X <= a.n2;
-    constexpr unsigned kBoxBytes = BX0<T> * BY0 * sizeof(T);
-    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned box start
-
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
-        for (int w = 0; w < NLY; ++w) prog[w] = 0;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        prefetch_tmap(&tmap);
-    }
-    __syncthreads();  // the only CTA-wide barrier
 
     // Columns owned: region-1 (y, x) = (VY*ly + cy, VX*lx + cx).
     const int x = VX * lx, y = VY * ly;
@@ -287,6 +250,21 @@ __global__ void __launch_bounds__(NT, 1)
                            x + cx >= HX && x + cx < HX + TX;
         }
 
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&tmap);
+    }
+    __syncthreads();
+    constexpr unsigned kBoxBytes = BX0<T> * BY0 * sizeof(T);
+    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned box start
+    if (tid == 0) {
+        for (int s = 0; s < STAGES && s < niter; ++s) {
+            mbar_expect_tx(&bar[s], kBoxBytes);
+            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + s);
+        }
+    }
+
     T Hs[K][3][VY][VX];
 #pragma unroll
     for (int l = 0; l < K; ++l)
@@ -297,43 +275,16 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) Hs[l][s][cy][cx] = T(0);
 
-    // Plane step `it` reads the rows the a1-neighbour warps wrote in step it-1
-    // and overwrites level buffers they read in step it-2: wait for both
-    // neighbours to have finished step it-1 (3-deep buffers make that enough).
-    // TMA ring pump, run by lane 0 of warp 0: plane j goes into slot
-    // j % STAGES once every warp has finished step j-STAGES+1 (the last step
-    // reading the slot's previous plane).  It issues whatever is free and
-    // blocks only while the plane its own warp needs next is not issued yet;
-    // all earlier planes are issued by then, so the other warps can always
-    // reach the steps it waits for.
-    int next_issue = 0;
-    auto pump = [&](int need) {  // need: planes [0, need) must be issued
-        while (next_issue < niter) {
-            if (next_issue >= STAGES) {
-                const int req = next_issue - STAGES + 2;
-                bool free_slot = true;
-                for (int w = 0; w < NLY && free_slot; ++w) free_slot = ld_acquire(&prog[w]) >= req;
-                if (!free_slot) {
-                    if (next_issue >= need) break;
-                    __nanosleep(32);
-                    continue;
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            }
-            const int s = next_issue % STAGES;
-            mbar_expect_tx(&bar[s], kBoxBytes);
-            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + next_issue);
-            ++next_issue;
-        }
-    };
-    auto before = [&](int it) {
-        if (tid == 0) pump(it + 1);
-        if (ly > 0) wait_progress(&prog[ly - 1], it);
-        if (ly < NLY - 1) wait_progress(&prog[ly + 1], it);
-    };
     auto after = [&](int it) {
-        __syncwarp();
-        if (lx == 0) st_release(&prog[ly], it + 1);
+        __syncthreads();
+        // Plane t-1's slot is free: refill it with plane t-1+STAGES.
+        if (tid == 0 && it >= 1 && it - 1 + STAGES < niter) {
+            const int s = (it - 1) % STAGES;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[s], kBoxBytes);
+            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1,
+                           a.h0 + t_begin + it - 1 + STAGES);
+        }
     };
     // Planes t-K..t-1 all interior and the tile clear of the a1/a2 boundary:
     // no Dirichlet selects needed in this step (warp-uniform).
@@ -341,14 +292,13 @@ __global__ void __launch_bounds__(NT, 1)
         const int t = t_begin + it;
         return tile_int && t - K >= 0 && t - 1 < a.n0;
     };
-#define TB3D_STEP(PH, IT)                                                                     \
-    before(IT);                                                                               \
-    if (clear(IT))                                                                            \
-        tb3d_step<T, K, EXACT, PH, false>(a, out, ring, lev, bar, IT, t_begin, tb3, i0, i1,   \
-                                          lx, x, y, gx, gy, tile_int, cint, cout, Hs);        \
-    else                                                                                      \
-        tb3d_step<T, K, EXACT, PH, true>(a, out, ring, lev, bar, IT, t_begin, tb3, i0, i1,    \
-                                         lx, x, y, gx, gy, tile_int, cint, cout, Hs);         \
+#define TB3D_STEP(PH, IT)                                                                    \
+    if (clear(IT))                                                                           \
+        tb3d_step<T, K, EXACT, PH, false>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x, \
+                                          y, gx, gy, tile_int, cint, cout, Hs);              \
+    else                                                                                     \
+        tb3d_step<T, K, EXACT, PH, true>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x,  \
+                                         y, gx, gy, tile_int, cint, cout, Hs);               \
     after(IT);
     for (int it = 0; it < niter; it += 3) {
         TB3D_STEP(0, it)
