@@ -120,7 +120,7 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 template <typename T, int K, bool EXACT, int PH, bool SEL>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
                                           uint64_t* bar, int it, int t_begin, int i0, int i1,
-                                          int lx, int x, int y, int gx, int gy, bool tile_int,
+                                          int lx, int x, int y, int gx, int gy,
                                           const bool (&cint)[VY][VX], const bool (&cout)[VY][VX],
                                           T (&Hs)[K][3][VY][VX]) {
     using P2 = typename Pair<T>::type;
@@ -235,7 +235,6 @@ __global__ void __launch_bounds__(NT, 1)
     const int i1 = min(i0 + a.chunk, a.n0);
     const int t_begin = i0 - K, t_end = i1 + K;
     const int niter = t_end - t_begin;
-    const bool tile_int = gy >= 0 && gy + R1Y <= a.n1 && gx >= 0 && gx + R1X <= a.n2;
 
     // Columns owned: region-1 (y, x) = (VY*ly + cy, VX*lx + cx).
     const int x = VX * lx, y = VY * ly;
@@ -286,19 +285,25 @@ __global__ void __launch_bounds__(NT, 1)
                            a.h0 + t_begin + it - 1 + STAGES);
         }
     };
-    // Planes t-K..t-1 all interior and the tile clear of the a1/a2 boundary:
-    // no Dirichlet selects needed in this step (warp-uniform).
+    // Planes t-K..t-1 all interior and no column of this warp on the a1/a2
+    // boundary: no Dirichlet selects needed in this step (warp-uniform).
+    bool mine = true;
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) mine &= cint[cy][cx];
+    const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in this warp
     auto clear = [&](int it) {
         const int t = t_begin + it;
-        return tile_int && t - K >= 0 && t - 1 < a.n0;
+        return warp_int && t - K >= 0 && t - 1 < a.n0;
     };
 #define TB3D_STEP(PH, IT)                                                                    \
     if (clear(IT))                                                                           \
         tb3d_step<T, K, EXACT, PH, false>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x, \
-                                          y, gx, gy, tile_int, cint, cout, Hs);              \
+                                          y, gx, gy, cint, cout, Hs);              \
     else                                                                                     \
         tb3d_step<T, K, EXACT, PH, true>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x,  \
-                                         y, gx, gy, tile_int, cint, cout, Hs);               \
+                                         y, gx, gy, cint, cout, Hs);               \
     after(IT);
     for (int it = 0; it < niter; it += 3) {
         TB3D_STEP(0, it)
