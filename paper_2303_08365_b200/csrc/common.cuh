@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <string>
+#include <type_traits>
 
 #include "../../include/tessera_b200.h"
 
@@ -101,6 +102,29 @@ __device__ __forceinline__ float madd(float acc, float w, float x) {
 template <bool EXACT, typename T>
 __device__ __forceinline__ T first(T w, T x) {
     return madd<EXACT>(T(0), w, x);
+}
+
+// Leading tap without the "0 +": the reference's accumulator starts at +0 and
+// can never become -0 (x + y is -0 only if both are -0), so a sum started
+// from the first product differs from it at most in the sign of a zero
+// result — in intermediate fused levels too, because a signed zero addend
+// never changes a nonzero sum.  Engines that use lead() apply fix_zero() to
+// every value they store, restoring the reference bit pattern exactly.
+__device__ __forceinline__ double lead(double w, double x) { return __dmul_rn(w, x); }
+__device__ __forceinline__ float lead(float w, float x) { return __fmul_rn(w, x); }
+template <bool EXACT, typename T>
+__device__ __forceinline__ T fix_zero(T v) {
+    if constexpr (EXACT) return v + T(0);
+    else return v;
+}
+
+// Compile-time loop: f(std::integral_constant<int, i>) for i in [0, N).
+template <int I, int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for<I + 1, N>(f);
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -136,77 +136,94 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
         load_row<T, V>(base_in + r * a.pitch, row_ok(r), pf[s]);
     }
 
-    for (int64_t tb = t_start; tb < t_end; tb += P) {
+    bool mine = true;
 #pragma unroll
-        for (int ph = 0; ph < P; ++ph) {
-            const int64_t t = tb + ph;
-            if (t < t_end) {
-                // Level 0: take row t from the prefetch ring, refill the slot.
-#pragma unroll
-                for (int v = 0; v < V; ++v) win[0][ph][R + v] = pf[ph][v];
-                {
-                    const int64_t r = t + P;
-                    load_row<T, V>(base_in + r * a.pitch, row_ok(r) && r < t_end, pf[ph]);
-                }
-                if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
+    for (int v = 0; v < V; ++v) mine &= cint[v];
+    const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in the strip
 
-                // Levels 1..K: level l produces row x = t - l*R.
+    // One row step: level 0 takes row t, level l produces row t - l*R.
+    // SEL = false is the select-free instantiation for steps where every
+    // produced row and every column of the warp is interior.
+    auto step = [&](auto PHc, auto SELc, int64_t t) {
+        constexpr int ph = decltype(PHc)::value;
+        constexpr bool SEL = decltype(SELc)::value;
 #pragma unroll
-                for (int l = 1; l <= K; ++l) {
-                    const int64_t x = t - (int64_t)l * R;
-                    const int sx = ((ph - l * R) % P + P) % P;  // slot of row x (static)
+        for (int v = 0; v < V; ++v) win[0][ph][R + v] = pf[ph][v];
+        {
+            const int64_t r = t + P;
+            load_row<T, V>(base_in + r * a.pitch, row_ok(r) && r < t_end, pf[ph]);
+        }
+        if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
+#pragma unroll
+        for (int l = 1; l <= K; ++l) {
+            const int64_t x = t - (int64_t)l * R;
+            const int sx = ((ph - l * R) % P + P) % P;  // slot of row x (static)
+            // Star taps read lane-halo columns of the centre row only:
+            // exchange it at use, so the halos of the other rows never
+            // occupy registers.  Box rows carry halos from production.
+            if constexpr (!BOX) exchange<T, V, R>(win[l - 1][sx]);
+            T res[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                T acc = T(0);
+                int tap = 0;
+#pragma unroll
+                for (int dr = -R; dr <= R; ++dr) {
+                    const int sr = ((sx + dr) % P + P) % P;
+#pragma unroll
+                    for (int dc = -R; dc <= R; ++dc) {
+                        if (has_tap<R, BOX>(dr, dc)) {
+                            const T xv = win[l - 1][sr][R + v + dc];
+                            acc = tap == 0 ? lead(a.w[0], xv) : madd<EXACT>(acc, a.w[tap], xv);
+                            ++tap;
+                        }
+                    }
+                }
+                if constexpr (SEL) {
                     const bool rint = x >= 0 && x < a.rows;
-                    // Star taps read lane-halo columns of the centre row only:
-                    // exchange it at use, so the halos of the other rows never
-                    // occupy registers.  Box rows carry halos from production.
-                    if constexpr (!BOX) exchange<T, V, R>(win[l - 1][sx]);
-                    T res[V];
+                    res[v] = (rint && cint[v]) ? acc : win[l - 1][sx][R + v];
+                } else {
+                    res[v] = acc;
+                }
+            }
+            if (l < K) {
 #pragma unroll
-                    for (int v = 0; v < V; ++v) {
-                        T acc = T(0);
-                        int tap = 0;
+                for (int v = 0; v < V; ++v) win[l][sx][R + v] = res[v];
+                if constexpr (BOX) exchange<T, V, R>(win[l][sx]);
+            } else if (x >= rb && x < re) {
 #pragma unroll
-                        for (int dr = -R; dr <= R; ++dr) {
-                            const int sr = ((sx + dr) % P + P) % P;
+                for (int v = 0; v < V; ++v) res[v] = fix_zero<EXACT>(res[v]);
+                T* dst = base_out + x * a.pitch;
+                if (all_out) {
+                    if constexpr (sizeof(T) * V == 16) {
+                        typename Vec<T, V>::type o;
+                        T* os = reinterpret_cast<T*>(&o);
 #pragma unroll
-                            for (int dc = -R; dc <= R; ++dc) {
-                                if (has_tap<R, BOX>(dr, dc)) {
-                                    const T xv = win[l - 1][sr][R + v + dc];
-                                    acc = tap == 0 ? first<EXACT>(a.w[0], xv)
-                                                   : madd<EXACT>(acc, a.w[tap], xv);
-                                    ++tap;
-                                }
-                            }
-                        }
-                        const T keep = win[l - 1][sx][R + v];
-                        res[v] = (rint && cint[v]) ? acc : keep;
+                        for (int v = 0; v < V; ++v) os[v] = res[v];
+                        *reinterpret_cast<typename Vec<T, V>::type*>(dst) = o;
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) dst[v] = res[v];
                     }
-                    if (l < K) {
+                } else {
 #pragma unroll
-                        for (int v = 0; v < V; ++v) win[l][sx][R + v] = res[v];
-                        if constexpr (BOX) exchange<T, V, R>(win[l][sx]);
-                    } else if (x >= rb && x < re) {
-                        T* dst = base_out + x * a.pitch;
-                        if (all_out) {
-                            if constexpr (sizeof(T) * V == 16) {
-                                typename Vec<T, V>::type o;
-                                T* os = reinterpret_cast<T*>(&o);
-#pragma unroll
-                                for (int v = 0; v < V; ++v) os[v] = res[v];
-                                *reinterpret_cast<typename Vec<T, V>::type*>(dst) = o;
-                            } else {
-#pragma unroll
-                                for (int v = 0; v < V; ++v) dst[v] = res[v];
-                            }
-                        } else {
-#pragma unroll
-                            for (int v = 0; v < V; ++v)
-                                if (cout[v]) dst[v] = res[v];
-                        }
-                    }
+                    for (int v = 0; v < V; ++v)
+                        if (cout[v]) dst[v] = res[v];
                 }
             }
         }
+    };
+
+    for (int64_t tb = t_start; tb < t_end; tb += P) {
+        static_for<0, P>([&](auto PHc) {
+            const int64_t t = tb + decltype(PHc)::value;
+            if (t < t_end) {
+                if (warp_int && t - (int64_t)K * R >= 0 && t - R < a.rows)
+                    step(PHc, std::false_type{}, t);
+                else
+                    step(PHc, std::true_type{}, t);
+            }
+        });
     }
 }
 
