@@ -33,7 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    "c1": dict(bench="Heat-2D", extent=[4096, 4096], dtype="f64", steps=100, fused=8,
+    "c1": dict(bench="Heat-2D", extent=[4096, 4096], dtype="f64", steps=100, fused=6,
                mode="exact", workload="C1: 2D heat 5-point star fp64, 4096x4096, 100 timesteps",
                ref_tile=[200, 200], ref_tb=50),
     "c2": dict(bench="Box-2D9P", extent=[16384, 16384], dtype="f64", steps=100, fused=4,

@@ -138,6 +138,12 @@ class _DeviceState:
         start = (row + self.h0) * self.plane
         return self.dg.buf[self.dg.cur][start:start + count * self.plane]
 
+    def sync(self):
+        self.dg.torch.cuda.current_stream(self.dg.device).synchronize()
+
+    def download(self, host_local):
+        self.dg.download(host_local)
+
 
 class _HostState:
     """Local slab on the host stepped by an injected CPU engine (tests only:
@@ -162,6 +168,9 @@ class _HostState:
         start = (row + self.h0) * self.plane
         return self.torch.from_numpy(self.g.read_data()[start:start + count * self.plane])
 
+    def sync(self):
+        pass
+
 
 class SlabRunner:
     """Round driver for one rank (HaloWorker::run_round generalised to P
@@ -171,6 +180,11 @@ class SlabRunner:
     def __init__(self, plan: SlabPlan, state, group=None):
         import torch.distributed as dist
         self.dist = dist
+        # gloo cannot move CUDA tensors point-to-point: stage through host
+        # memory (tests run several ranks on one GPU this way); NCCL sends
+        # straight from HBM.
+        self.stage_via_host = (dist.is_initialized() and
+                               dist.get_backend(group) == "gloo")
         self.plan = plan
         self.state = state
         self.group = group
@@ -214,25 +228,34 @@ class SlabRunner:
         """One message per direction per seam (scheduler.cpp:371-381)."""
         p, dist = self.plan, self.dist
         d = p.depth
-        ops = []
+        sends, recvs = [], []  # (peer, tensor)
         if p.rank > 0:
-            ops.append(dist.P2POp(dist.isend, self.state.planes(p.ghost_lo, d), p.rank - 1,
-                                  self.group))
-            ops.append(dist.P2POp(dist.irecv, self.state.planes(0, d), p.rank - 1, self.group))
+            sends.append((p.rank - 1, self.state.planes(p.ghost_lo, d)))
+            recvs.append((p.rank - 1, self.state.planes(0, d)))
             self.log.records.append(CommRecord(self.round, f"r{p.rank - 1}_to_r{p.rank}",
                                                p.bytes_per_message))
         if p.rank < p.world - 1:
-            ops.append(dist.P2POp(dist.isend, self.state.planes(p.ghost_lo + p.own - d, d),
-                                  p.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, self.state.planes(p.ghost_lo + p.own, d),
-                                  p.rank + 1, self.group))
+            sends.append((p.rank + 1, self.state.planes(p.ghost_lo + p.own - d, d)))
+            recvs.append((p.rank + 1, self.state.planes(p.ghost_lo + p.own, d)))
             self.log.records.append(CommRecord(self.round, f"r{p.rank + 1}_to_r{p.rank}",
                                                p.bytes_per_message))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
-            for op in ops[::2]:
-                self.exchange_bytes += op.tensor.numel() * op.tensor.element_size()
+        if not sends:
+            return
+        staged = None
+        if self.stage_via_host and sends[0][1].is_cuda:
+            self.state.sync()
+            sends = [(peer, t.cpu()) for peer, t in sends]
+            staged = recvs
+            recvs = [(peer, t.new_empty(t.shape, device="cpu")) for peer, t in recvs]
+        ops = [dist.P2POp(dist.isend, t, peer, self.group) for peer, t in sends]
+        ops += [dist.P2POp(dist.irecv, t, peer, self.group) for peer, t in recvs]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        if staged is not None:
+            for (peer, dst), (_, src) in zip(staged, recvs):
+                dst.copy_(src)
+        for _, t in sends:
+            self.exchange_bytes += t.numel() * t.element_size()
 
     def advance(self, n: int):
         if n > self.fused_steps:
@@ -256,10 +279,14 @@ class SlabRunner:
             self.advance(n)
             left -= n
 
-    def own_rows(self):
-        """Owned rows of the local read buffer as a padded-shape ndarray
-        (host state only)."""
-        g = self.state.g
+    def own_rows(self, host_local=None):
+        """Owned rows of the local read buffer as a padded-shape ndarray (a
+        device state is first downloaded into `host_local`)."""
+        if host_local is not None:
+            self.state.download(host_local)
+            g = host_local
+        else:
+            g = self.state.g
         h0 = g.halo[0]
         return g.padded(g.parity)[h0 + self.plan.ghost_lo:h0 + self.plan.ghost_lo + self.plan.own]
 

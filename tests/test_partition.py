@@ -89,3 +89,52 @@ def test_reference_message_and_ghost_counts(ts, orc, tmp_path):
     assert p0.local_extent == [67, 64] and p1.local_extent == [67, 64]
     with pytest.raises(ValueError):
         plan_slabs([8, 8], 1, 5, 2, 0)  # subdomain smaller than the halo depth
+
+
+def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    import oracle
+    import paper_2303_08365_b200 as ts
+    from paper_2303_08365_b200.partition import SlabRunner, local_from_global, plan_slabs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    orc = oracle.Oracle()
+    kern = ts.find_benchmark(name).kernel
+    glob = ts.Grid(extent, [kern.radius] * len(extent))
+    orc.fill_random(glob, 500)
+    plan = plan_slabs(extent, kern.radius, k, world, rank)
+    loc = local_from_global(glob, plan, poison=True)
+    runner = SlabRunner.on_device(ts, kern, plan, loc, torch.device("cuda", 0))
+    runner.run(steps)
+    np.save(os.path.join(out_dir, f"own{rank}.npy"), runner.own_rows(loc))
+    np.save(os.path.join(out_dir, f"log{rank}.npy"),
+            np.array([len(runner.log.records), runner.round, runner.log.ghost_recompute_points]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,name,extent,steps,k", [
+    (2, "Heat-3D", [70, 40, 67], 7, 3),   # tb3d engine on each slab
+    (3, "Box-2D9P", [90, 130], 9, 4),    # stream2d engine
+    (2, "Box-3D27P", [40, 30, 50], 4, 1),  # box3d engine
+])
+def test_slabs_on_device_equal_oracle(ts, orc, tmp_path, world, name, extent, steps, k):
+    """The device slab state (pitched HBM buffers, tsr_advance, zero-copy
+    plane views) with several ranks sharing one GPU over gloo."""
+    port = _free_port()
+    mp.start_processes(_gpu_worker, args=(world, port, name, extent, steps, k, str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    kern = ts.find_benchmark(name).kernel
+    ref = ts.Grid(extent, [kern.radius] * len(extent))
+    orc.fill_random(ref, 500)
+    orc.naive_run(ref, kern, steps)
+    h = kern.radius
+    got = np.concatenate([np.load(tmp_path / f"own{r}.npy") for r in range(world)], axis=0)
+    want = ref.padded(ref.parity)[h:h + extent[0]]
+    assert np.isfinite(got).all()
+    assert got.tobytes() == want.tobytes()
