@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--mode", default=None, choices=["exact", "fast"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the N>1 path with ranks sharing one GPU")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     args.steps = cfg["steps"] if args.steps is None else args.steps
@@ -228,12 +230,19 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    ndev = torch.cuda.device_count()
+    if args.dist_backend == "nccl" and world > ndev:
+        raise SystemExit(f"--gpus {world} but only {ndev} CUDA devices are visible")
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     mode = args.mode or cfg["mode"]
     fused_req = cfg["fused"] if args.fused is None else args.fused
@@ -260,7 +269,7 @@ def main():
         glob = [per_gpu[0] * world] + per_gpu[1:]
         plan = plan_slabs(glob, k.radius, kfused_guess, world, rank)
         runner = SlabRunner.synthetic(ts, k, plan, cfg["dtype"], dev, seed=1 + rank,
-                                      fused_steps=kfused_guess, mode=mode)
+                                      fused_steps=fused_req, mode=mode)
         kfused = runner.fused_steps
         engine = 2
         advance = runner.advance
@@ -291,10 +300,11 @@ def main():
     full = [ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(groups) if n == kfused]
     launch_ms = statistics.mean(full) if full else elapsed_ms / max(1, len(groups))
     if dist:
-        t = torch.tensor([elapsed_ms, launch_ms], device=dev, dtype=torch.float64)
+        rdev = dev if args.dist_backend == "nccl" else "cpu"
+        t = torch.tensor([elapsed_ms, launch_ms], device=rdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms, launch_ms = float(t[0]), float(t[1])
-        lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+        lt = torch.tensor([launches], device=rdev, dtype=torch.int64)
         dist.all_reduce(lt)
         launches = int(lt[0])
 
