@@ -91,25 +91,11 @@ __device__ __forceinline__ void exchange(T (&row)[V + 2 * R]) {
     }
 }
 
-// Tap index in canonical (dr, dc) lexicographic order.
-template <int R, bool BOX>
-__host__ __device__ constexpr int tap_index(int dr, int dc) {
-    if (BOX) return (dr + R) * (2 * R + 1) + (dc + R);
-    if (dr < 0) return dr + R;
-    if (dr == 0) return R + (dc + R);
-    return 3 * R + dr;
-}
-
-// Row-contribution streaming.  When row q of level l-1 arrives, it
-// contributes its dr-taps to every level-l output row x = q - dr, dr = -R..R:
-// x = q+R starts (first tap), x = q-R completes.  Each output therefore sums
-// its taps in the oracle's (dr, dc) order, and a level carries only 2R+1
-// accumulator rows (slot x mod (2R+1)) instead of a window of input rows.
 template <typename T, int R, bool BOX, int K, int V, bool EXACT>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     const T* __restrict__ in, T* __restrict__ out, const __grid_constant__ S2Args<T> a) {
-    constexpr int M = 2 * R + 1;  // accumulator slots per level (= rows per phase period)
-    constexpr int W = V + 2 * R;  // values of an arriving row incl. lane halo
+    constexpr int P = 2 * R + 1;  // ring depth per level
+    constexpr int W = V + 2 * R;  // values per ring row incl. lane halo
     const int lane = threadIdx.x & 31;
     const int64_t gw = blockIdx.x * (int64_t)kWarpsPerBlock + (threadIdx.x >> 5);
     if (gw >= a.total_warps) return;
@@ -122,124 +108,117 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     const int64_t c0 = ob - a.hl + (int64_t)lane * V;  // this lane's first column
     const bool col_alloc = c0 >= a.col_lo && c0 + V <= a.col_hi;
 
+    // Per-value column masks (constant down the strip).
     bool cint[V], cout[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
         cint[v] = c0 + v >= 0 && c0 + v < a.cols;
         cout[v] = c0 + v >= ob && c0 + v < oe;
     }
-    bool all_out = true, mine = true;
+    bool all_out = true;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-        all_out &= cout[v];
-        mine &= cint[v];
-    }
-    const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in the strip
+    for (int v = 0; v < V; ++v) all_out &= cout[v];
 
-    T acc[K][M][V];  // level l (1..K) accumulator of output row x in slot x % M
-    T pf[M][V];      // prefetch ring of level-0 rows
+    T win[K][P][W];  // ring of rows per level (level K is stored, not kept)
+    T pf[P][V];      // prefetch ring of level-0 rows
 
     const int64_t t_start = rb - (int64_t)K * R;
     const int64_t t_end = re + (int64_t)K * R;  // exclusive
     const T* base_in = in + a.origin + c0;
     T* base_out = out + a.origin + c0;
+
     auto row_ok = [&](int64_t r) { return r >= -a.hrow && r < a.rows + a.hrow && col_alloc; };
 
+    // Prime the prefetch ring with rows t_start .. t_start+P-1.
 #pragma unroll
-    for (int s = 0; s < M; ++s) {
+    for (int s = 0; s < P; ++s) {
         const int64_t r = t_start + s;
         load_row<T, V>(base_in + r * a.pitch, row_ok(r), pf[s]);
     }
-#pragma unroll
-    for (int l = 0; l < K; ++l)
-#pragma unroll
-        for (int s = 0; s < M; ++s)
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[l][s][v] = T(0);
 
-    // One step: level-0 row t arrives; level l receives row q = t-(l-1)R of
-    // level l-1 and completes its row t-lR.  Slots are static: the step loop
-    // is unrolled by M and slot(x) = (x - t_start) mod M.
+    bool mine = true;
+#pragma unroll
+    for (int v = 0; v < V; ++v) mine &= cint[v];
+    const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in the strip
+
+    // One row step: level 0 takes row t, level l produces row t - l*R.
+    // SEL = false is the select-free instantiation for steps where every
+    // produced row and every column of the warp is interior.
     auto step = [&](auto PHc, auto SELc, int64_t t) {
         constexpr int ph = decltype(PHc)::value;
         constexpr bool SEL = decltype(SELc)::value;
-        T row[W];  // the arriving row of level l-1, with lane halo
 #pragma unroll
-        for (int v = 0; v < V; ++v) row[R + v] = pf[ph][v];
+        for (int v = 0; v < V; ++v) win[0][ph][R + v] = pf[ph][v];
         {
-            const int64_t r = t + M;
+            const int64_t r = t + P;
             load_row<T, V>(base_in + r * a.pitch, row_ok(r) && r < t_end, pf[ph]);
         }
+        if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
 #pragma unroll
         for (int l = 1; l <= K; ++l) {
-            exchange<T, V, R>(row);
-            const int64_t q = t - (int64_t)(l - 1) * R;  // arriving row index
-            T done[V];
+            const int64_t x = t - (int64_t)l * R;
+            const int sx = ((ph - l * R) % P + P) % P;  // slot of row x (static)
+            // Star taps read lane-halo columns of the centre row only:
+            // exchange it at use, so the halos of the other rows never
+            // occupy registers.  Box rows carry halos from production.
+            if constexpr (!BOX) exchange<T, V, R>(win[l - 1][sx]);
+            T res[V];
 #pragma unroll
-            for (int dr = -R; dr <= R; ++dr) {
-                const int64_t x = q - dr;                           // output row
-                const int sl = ((ph - (l - 1) * R - dr) % M + M) % M;  // slot of x (static)
-                bool rfr = false;
-                if constexpr (SEL) rfr = !(x >= 0 && x < a.rows);
+            for (int v = 0; v < V; ++v) {
+                T acc = T(0);
+                int tap = 0;
 #pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    T s = acc[l - 1][sl][v];
+                for (int dr = -R; dr <= R; ++dr) {
+                    const int sr = ((sx + dr) % P + P) % P;
 #pragma unroll
                     for (int dc = -R; dc <= R; ++dc) {
                         if (has_tap<R, BOX>(dr, dc)) {
-                            const int ti = tap_index<R, BOX>(dr, dc);
-                            const T xv = row[R + v + dc];
-                            s = ti == 0 ? lead(a.w[0], xv) : madd<EXACT>(s, a.w[ti], xv);
+                            const T xv = win[l - 1][sr][R + v + dc];
+                            acc = tap == 0 ? lead(a.w[0], xv) : madd<EXACT>(acc, a.w[tap], xv);
+                            ++tap;
                         }
                     }
-                    if constexpr (SEL) {
-                        // Dirichlet: a frozen output keeps its level-(l-1)
-                        // value, i.e. the arriving row's cell when dr == 0.
-                        const bool frz = rfr || !cint[v];
-                        if (dr == 0) s = frz ? row[R + v] : s;
-                        else if (dr != -R) s = frz ? acc[l - 1][sl][v] : s;
-                    }
-                    if (dr == R) done[v] = s;
-                    else acc[l - 1][sl][v] = s;
+                }
+                if constexpr (SEL) {
+                    const bool rint = x >= 0 && x < a.rows;
+                    res[v] = (rint && cint[v]) ? acc : win[l - 1][sx][R + v];
+                } else {
+                    res[v] = acc;
                 }
             }
-            // level l row t - lR is complete
             if (l < K) {
 #pragma unroll
-                for (int v = 0; v < V; ++v) row[R + v] = done[v];
-            } else {
-                const int64_t x = t - (int64_t)K * R;
-                if (x >= rb && x < re) {
+                for (int v = 0; v < V; ++v) win[l][sx][R + v] = res[v];
+                if constexpr (BOX) exchange<T, V, R>(win[l][sx]);
+            } else if (x >= rb && x < re) {
 #pragma unroll
-                    for (int v = 0; v < V; ++v) done[v] = fix_zero<EXACT>(done[v]);
-                    T* dst = base_out + x * a.pitch;
-                    if (all_out) {
-                        if constexpr (sizeof(T) * V == 16) {
-                            typename Vec<T, V>::type o;
-                            T* os = reinterpret_cast<T*>(&o);
+                for (int v = 0; v < V; ++v) res[v] = fix_zero<EXACT>(res[v]);
+                T* dst = base_out + x * a.pitch;
+                if (all_out) {
+                    if constexpr (sizeof(T) * V == 16) {
+                        typename Vec<T, V>::type o;
+                        T* os = reinterpret_cast<T*>(&o);
 #pragma unroll
-                            for (int v = 0; v < V; ++v) os[v] = done[v];
-                            *reinterpret_cast<typename Vec<T, V>::type*>(dst) = o;
-                        } else {
-#pragma unroll
-                            for (int v = 0; v < V; ++v) dst[v] = done[v];
-                        }
+                        for (int v = 0; v < V; ++v) os[v] = res[v];
+                        *reinterpret_cast<typename Vec<T, V>::type*>(dst) = o;
                     } else {
 #pragma unroll
-                        for (int v = 0; v < V; ++v)
-                            if (cout[v]) dst[v] = done[v];
+                        for (int v = 0; v < V; ++v) dst[v] = res[v];
                     }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        if (cout[v]) dst[v] = res[v];
                 }
             }
         }
     };
 
-    for (int64_t tb = t_start; tb < t_end; tb += M) {
-        static_for<0, M>([&](auto PHc) {
+    for (int64_t tb = t_start; tb < t_end; tb += P) {
+        static_for<0, P>([&](auto PHc) {
             const int64_t t = tb + decltype(PHc)::value;
             if (t < t_end) {
-                // rows touched this step: [t - K*R, t + R]
-                if (warp_int && t - (int64_t)K * R >= 0 && t + R < a.rows)
+                if (warp_int && t - (int64_t)K * R >= 0 && t - R < a.rows)
                     step(PHc, std::false_type{}, t);
                 else
                     step(PHc, std::true_type{}, t);
