@@ -15,6 +15,7 @@ from .run import (GpuStats, TilePlan, naive_run, naive_step, plan_tiles, run_gpu
                   run_tessellated)
 from .metrics import RateReport, deviation, max_abs, max_rel_deviation, stencils_per_second
 from .device import DeviceGrid, layout_of
+from .harness import csv_header, csv_row, run_all, run_benchmark, write_csv
 
 __version__ = "0.1.0"
 
@@ -24,5 +25,6 @@ __all__ = [
     "BasicGrid", "Grid", "GridF", "dump_grid", "fill_random", "grid_from_numpy", "load_grid",
     "GpuStats", "TilePlan", "naive_run", "naive_step", "plan_tiles", "run_gpu",
     "run_tessellated", "RateReport", "deviation", "max_abs", "max_rel_deviation",
-    "stencils_per_second", "DeviceGrid", "layout_of",
+    "stencils_per_second", "DeviceGrid", "layout_of", "run_benchmark", "run_all", "csv_header",
+    "csv_row", "write_csv",
 ]

@@ -1,0 +1,138 @@
+"""Benchmark harness of the reference (proj/include/tessera/bench.hpp,
+proj/src/bench.cpp:63-312) with the GPU sweep as its executor path.
+
+``run_benchmark(name, path="gpu", scale="desk", threads=1, seed=1, steps=0)``
+returns the same dict as the reference binding (proj/bindings/module.cpp:
+385-409) plus GPU columns.  As in the reference (bench.cpp:248-260) a row is
+first verified at a reduced size, then timed at desk or full scale:
+
+* paths ``gpu`` (engine's fused depth), ``tessellate`` (k = the Table-1 tb,
+  clamped like clamp_tb, bench.cpp:104-107) and ``naive`` (k = 1) run on the
+  B200; ``vector``/``mm``/``hetero`` are CPU simulators of the reference and
+  report ``unsupported``, like its unsupported path/dimension pairings;
+* verify compares the tuned engine with the one-thread-per-point generic GPU
+  engine (an independent implementation of apply_box; the product never
+  calls the CPU oracle) and requires max_rel_deviation <= 1e-12, the
+  reference's tolerance;
+* ``elapsed_s`` is the wall time of the reference-facing call (host buffers
+  in and out, as the reference times execute_path); ``device_s`` is the CUDA
+  event time of the sweeps alone.
+"""
+from __future__ import annotations
+
+import time
+
+from .grid import Grid, fill_random
+from .kernel import benchmark_table, find_benchmark
+from .metrics import deviation, stencils_per_second
+from .run import run_gpu
+
+PATHS = ("gpu", "tessellate", "naive")
+CPU_ONLY = ("vector", "mm", "hetero")
+
+
+def clamp_tb(tb: int, min_tile: int, radius: int) -> int:
+    """bench.cpp:104-107."""
+    return max(1, min(tb, min_tile // (2 * radius)))
+
+
+def make_setup(spec, scale: str):
+    """bench.cpp:192-208 (desk: extents / 20, at least 8)."""
+    extent = list(spec.full_extent)
+    if scale == "desk":
+        extent = [max(e // 20, 8) for e in extent]
+    if spec.kernel.dims == 1:
+        extent = [(e + 3) // 4 * 4 for e in extent]
+    tile = [min(t, e) for t, e in zip(spec.tile, extent)]
+    return extent, tile, clamp_tb(spec.tb, min(tile), spec.kernel.radius)
+
+
+def verify_setup(spec):
+    """bench.cpp:210-226."""
+    dims, r = spec.kernel.dims, spec.kernel.radius
+    extent, tile = {1: ([256], [32]), 2: ([64, 64], [16, 16]), 3: ([24, 24, 24], [8, 8, 8])}[dims]
+    return extent, tile, clamp_tb(min(spec.tb, 3), tile[0], r)
+
+
+def _fused(path: str, tb: int) -> int:
+    return {"gpu": 0, "tessellate": tb, "naive": 1}[path]
+
+
+def run_benchmark(name: str, path: str = "gpu", scale: str = "desk", threads: int = 1,
+                  seed: int = 1, steps: int = 0, mode: str = "exact") -> dict:
+    spec = find_benchmark(name)
+    k = spec.kernel
+    row = {"name": spec.name, "path": path, "dims": k.dims, "extent": [], "T": 0, "tile": [],
+           "Tb": 0, "elapsed_s": 0.0, "stencils_per_s": 0.0, "verify": "skip", "seed": seed,
+           "ghost_recompute_points": 0, "mma_calls": 0, "messages": 0,
+           "gpus": 1, "k": 0, "device_s": 0.0, "achieved_GBps": 0.0, "roofline_frac": 0.0,
+           "max_abs_err": None, "l2_rel_err": None}
+    if path in CPU_ONLY:
+        row["verify"] = "unsupported"
+        return row
+    if path not in PATHS:
+        raise ValueError(f"unknown executor path: {path}")
+    if scale not in ("desk", "full"):
+        raise ValueError("scale must be 'desk' or 'full'")
+
+    # verify at the reduced size (T = 6), tuned path vs the generic engine
+    vext, _, vtb = verify_setup(spec)
+    probe = Grid(vext, [k.radius] * k.dims)
+    fill_random(probe, seed)
+    check = probe.copy()
+    run_gpu(probe, k, 6, fused_steps=_fused(path, vtb), mode=mode)
+    run_gpu(check, k, 6, engine="generic")
+    d = deviation(probe, check)
+    row["verify"] = "pass" if d["max_rel_deviation"] <= 1e-12 else "fail"
+    row["max_abs_err"], row["l2_rel_err"] = d["max_abs_err"], d["l2_rel_err"]
+
+    extent, tile, tb = make_setup(spec, scale)
+    t_steps = min(spec.full_steps, 1000) if scale == "desk" else spec.full_steps
+    if steps > 0:
+        t_steps = steps
+    row.update(extent=extent, tile=tile, Tb=tb, T=t_steps)
+    g = Grid(extent, [k.radius] * k.dims, pinned=True)
+    fill_random(g, seed)
+    t0 = time.perf_counter()
+    st = run_gpu(g, k, t_steps, fused_steps=_fused(path, tb), mode=mode)
+    elapsed = max(time.perf_counter() - t0, 1e-9)
+    rate = stencils_per_second(extent, t_steps, elapsed)
+    row.update(elapsed_s=elapsed, stencils_per_s=rate.stencils_per_second, k=st.fused_steps,
+               device_s=st.device_ms / 1e3)
+    if st.device_ms > 0:
+        dev_rate = rate.points_per_step * t_steps / (st.device_ms / 1e3)
+        row["achieved_GBps"] = dev_rate * 2 * 8 / 1e9
+        row["roofline_frac"] = row["achieved_GBps"] / 6548.8
+    return row
+
+
+CSV_FIELDS = ("name", "path", "dims", "extent", "T", "tile", "Tb", "elapsed_s",
+              "stencils_per_s", "verify", "seed", "ghost_recompute_points", "mma_calls",
+              "messages", "gpus", "k", "device_s", "achieved_GBps", "roofline_frac",
+              "max_abs_err", "l2_rel_err")
+
+
+def csv_header() -> str:
+    """The reference's 14 columns (bench.cpp:289-292) + the GPU columns."""
+    return ",".join(CSV_FIELDS)
+
+
+def csv_row(row: dict) -> str:
+    def fmt(key):
+        v = row.get(key)
+        if key in ("extent", "tile"):
+            return "x".join(str(e) for e in v)
+        return "" if v is None else str(v)
+    return ",".join(fmt(f) for f in CSV_FIELDS)
+
+
+def write_csv(path: str, rows) -> None:
+    with open(path, "w") as f:
+        f.write(csv_header() + "\n")
+        for r in rows:
+            f.write(csv_row(r) + "\n")
+
+
+def run_all(path: str = "gpu", scale: str = "desk", seed: int = 1) -> list:
+    """Every Table-1 benchmark on one path (the reference CLI's `bench run` loop)."""
+    return [run_benchmark(s.name, path=path, scale=scale, seed=seed) for s in benchmark_table()]

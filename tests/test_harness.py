@@ -1,0 +1,38 @@
+"""The reference's benchmark harness on the GPU path (bench.cpp:63-312)."""
+import pytest
+
+
+def test_setup_shapes_match_the_reference(ts):
+    """make_setup / verify_setup / clamp_tb arithmetic (bench.cpp:104-107,
+    192-226), incl. the golden row's 500x500 desk extent and tb=50
+    (tests/golden/bench_row_golden.csv)."""
+    from paper_2303_08365_b200 import harness as h
+    spec = ts.find_benchmark("Heat-2D")
+    assert h.make_setup(spec, "desk") == ([500, 500], [200, 200], 50)
+    assert h.make_setup(ts.find_benchmark("Heat-3D"), "desk") == ([51, 51, 51], [20, 20, 20], 10)
+    assert h.make_setup(ts.find_benchmark("Heat-1D"), "desk")[0] == [500000]
+    assert h.verify_setup(ts.find_benchmark("Box-3D27P")) == ([24, 24, 24], [8, 8, 8], 3)
+    assert h.clamp_tb(50, 200, 1) == 50 and h.clamp_tb(500, 8, 2) == 2
+
+
+def test_csv_schema_extends_the_reference(ts):
+    """The first 14 columns are the reference's CSV header (bench.cpp:289-292,
+    tests/golden/bench_row_golden.csv)."""
+    ref = ("name,path,dims,extent,T,tile,Tb,elapsed_s,stencils_per_s,verify,seed,"
+           "ghost_recompute_points,mma_calls,messages")
+    assert ts.csv_header().startswith(ref + ",")
+    row = ts.run_benchmark("Heat-2D", path="vector")
+    assert row["verify"] == "unsupported"
+    assert ts.csv_row(row).split(",")[:2] == ["Heat-2D", "vector"]
+    with pytest.raises(ValueError):
+        ts.run_benchmark("Heat-2D", path="warp-drive")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", ["gpu", "tessellate", "naive"])
+def test_benchmark_rows_verify_and_time(ts, path):
+    """tests/python/test_smoke.py:136-140 on every GPU path, all 8 kernels."""
+    for spec in ts.benchmark_table():
+        row = ts.run_benchmark(spec.name, path=path, steps=4, seed=7)
+        assert row["verify"] == "pass", row
+        assert row["stencils_per_s"] > 0 and row["T"] == 4 and row["k"] >= 1
