@@ -191,11 +191,195 @@ __global__ void __launch_bounds__(NT) box3d_kernel(T* __restrict__ out,
     }
 }
 
+// ---------------------------------------------------------------------------
+// K = 2: two time steps per HBM pass.  Level 1 is computed with the same
+// plane-partial sums on the whole 64 x 32 tile (the level-0 box carries one
+// extra cell of halo), written to a triple-buffered SMEM plane, and level 2
+// runs the plane-partial sums over those SMEM planes for the inner 62 x 30
+// cells.  One __syncthreads per plane: after the level-1 plane is published.
+// Dirichlet: level-1 cells outside the interior keep their level-0 value, so
+// level 2 reads exactly what a second apply_box sweep would.
+constexpr int L1X = OX, L1Y = OY;  // level-1 region = the 64 x 32 tile
+constexpr int BH = L1Y + 2;        // SMEM level-1 plane rows incl. 1-row border
+constexpr int NB = 2;              // level-1 plane buffers
+// Vector alignment: the region's left margin is one 16-B vector (so TMA box
+// starts stay 16-B aligned) and SMEM rows put region column x at x + PAD.
+template <typename T>
+constexpr int HX2 = PAD<T>;                                          // left margin
+template <typename T>
+constexpr int TX2 = (L1X - HX2<T> - 1) / PAD<T> * PAD<T>;            // output width
+constexpr int TY2 = L1Y - 2;                                         // output height
+template <typename T>
+constexpr int BWP = L1X + 2 * PAD<T>;                                // SMEM row pitch
+
+template <typename T>
+constexpr int b_bytes() {
+    return (BWP<T> * BH * (int)sizeof(T) + 127) / 128 * 128;
+}
+template <typename T>
+constexpr int smem2_bytes() {
+    return STAGES * slot_bytes<T>() + NB * b_bytes<T>() + STAGES * 8;
+}
+
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
+                                                      const __grid_constant__ CUtensorMap tmap,
+                                                      const __grid_constant__ BoxArgs<T> a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
+    constexpr int BE = b_bytes<T>() / (int)sizeof(T);
+    constexpr int BX = BXW<T>, PL = PAD<T>;
+    T* ring = reinterpret_cast<T*>(smem);
+    T* buf = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T>());
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>() + NB * b_bytes<T>());
+
+    const int tid = threadIdx.x;
+    const int lx = tid % NLX, ly = tid / NLX;
+    const int tile = blockIdx.x;
+    const int bx = tile % a.tiles_x;
+    const int by = (tile / a.tiles_x) % a.tiles_y;
+    const int bz = tile / (a.tiles_x * a.tiles_y);
+    constexpr int HX = HX2<T>, TX = TX2<T>, BW = BWP<T>;
+    const int gx = bx * TX - HX, gy = by * TY2 - 1;  // global coords of L1 cell (0, 0)
+    const int i0 = bz * a.chunk;
+    const int i1 = min(i0 + a.chunk, a.n0);
+    // level-0 planes i0-2 .. i1+1 feed level-2 outputs i0 .. i1-1
+    const int t_begin = i0 - 2, niter = i1 - i0 + 4;
+    const int x = VX * lx, y = VY * ly;
+
+    bool cint[VY][VX], cout[VY][VX];
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) {
+            const int ga1 = gy + y + cy, ga2 = gx + x + cx;
+            cint[cy][cx] = ga1 >= 0 && ga1 < a.n1 && ga2 >= 0 && ga2 < a.n2;
+            cout[cy][cx] = cint[cy][cx] && y + cy >= 1 && y + cy < L1Y - 1 && x + cx >= HX &&
+                           x + cx < HX + TX;
+        }
+    bool mine = true;
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) mine &= cint[cy][cx];
+    const bool warp_int = __all_sync(0xffffffffu, mine);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&tmap);
+    }
+    __syncthreads();
+    constexpr unsigned kBoxBytes = BX * BY * sizeof(T);
+    // level-0 box: L1 region plus one cell, 16-B aligned start
+    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;
+    if (tid == 0)
+        for (int s = 0; s < STAGES && s < niter; ++s) {
+            mbar_expect_tx(&bar[s], kBoxBytes);
+            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + s);
+        }
+
+    T a1A[VY][VX], a1B[VY][VX];  // level 1: outputs q+1 (started), q (in progress)
+    T a2A[VY][VX], a2B[VY][VX];  // level 2: outputs q (started), q-1 (in progress)
+    T keep0[VY][VX];             // level-0 centre of plane q-1 (frozen level-1 cells)
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx)
+            a1A[cy][cx] = a1B[cy][cx] = a2A[cy][cx] = a2B[cy][cx] = keep0[cy][cx] = T(0);
+
+    using V4 = typename VecT<T, 16 / sizeof(T)>::type;
+    constexpr int NV = 16 / sizeof(T);
+    auto read_nb = [&](const T* rowbase, int pitch, T(&nb)[VY + 2][VX + 2]) {
+#pragma unroll
+        for (int r = 0; r < VY + 2; ++r) {
+            const T* row = rowbase + (y + r) * pitch;
+            nb[r][0] = row[-1];
+#pragma unroll
+            for (int v = 0; v < VX; v += NV) {
+                const V4 vv = *reinterpret_cast<const V4*>(row + v);
+                const T* e = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+                for (int u = 0; u < NV; ++u) nb[r][1 + v + u] = e[u];
+            }
+            nb[r][VX + 1] = row[VX];
+        }
+    };
+
+    for (int it = 0; it < niter; ++it) {
+        const int q = t_begin + it;  // level-0 plane in the ring
+        const int slot = it % STAGES;
+        mbar_wait(&bar[slot], (it / STAGES) & 1);
+        const bool sel = !(warp_int && q - 2 >= 0 && q < a.n0);  // planes q-2..q
+        T nb[VY + 2][VX + 2];
+        read_nb(ring + slot * SLOT + PL + x, BX, nb);
+        // level 1: finish q-1, continue q, start q+1
+        apply9<EXACT, false>(a.w + 18, nb, a1B);
+        T l1[VY][VX];
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < VX; ++cx) {
+                l1[cy][cx] = a1B[cy][cx];
+                if (sel && !(cint[cy][cx] && q - 1 >= 0 && q - 1 < a.n0))
+                    l1[cy][cx] = keep0[cy][cx];
+                keep0[cy][cx] = nb[cy + 1][cx + 1];
+            }
+        apply9<EXACT, false>(a.w + 9, nb, a1A);
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < VX; ++cx) a1B[cy][cx] = a1A[cy][cx];
+        apply9<EXACT, true>(a.w, nb, a1A);
+        // publish level-1 plane q-1: cell (y, x) at row y+1, column x+PAD
+        T* B = buf + (((q - 1) % NB + NB) % NB) * BE;
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+            for (int v = 0; v < VX; v += NV) {
+                V4 vv;
+                T* e = reinterpret_cast<T*>(&vv);
+#pragma unroll
+                for (int u = 0; u < NV; ++u) e[u] = l1[cy][v + u];
+                *reinterpret_cast<V4*>(B + (y + cy + 1) * BW + x + PL + v) = vv;
+            }
+        __syncthreads();
+        // every thread has read plane q: its slot takes plane q + STAGES
+        if (tid == 0 && it + STAGES < niter) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[slot], kBoxBytes);
+            tma_load_3d(ring + slot * SLOT, &tmap, &bar[slot], c0, c1,
+                        a.h0 + t_begin + it + STAGES);
+        }
+        // level 2 on level-1 plane q-1: finish q-2, continue q-1, start q
+        T nb2[VY + 2][VX + 2];
+        read_nb(B + PL + x, BW, nb2);  // buffer rows y..y+VY+1 = region rows y-1..y+VY
+        apply9<EXACT, false>(a.w + 18, nb2, a2B);
+        const int po = q - 2;
+        if (it >= 4 && po < i1) {
+            // stored cells are interior (cout implies cint): no Dirichlet select
+            T* o = out + a.origin + (long long)po * a.pitch0 + (long long)(gy + y) * a.pitch1 +
+                   (gx + x);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx)
+                    if (cout[cy][cx]) o[cy * a.pitch1 + cx] = fix_zero<EXACT>(a2B[cy][cx]);
+        }
+        apply9<EXACT, false>(a.w + 9, nb2, a2A);
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < VX; ++cx) a2B[cy][cx] = a2A[cy][cx];
+        apply9<EXACT, true>(a.w, nb2, a2A);
+    }
+}
+
 bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
     if (t.dims != 3 || t.shape != TSR_BOX || t.radius != 1 || t.ntaps != 27) return false;
     if (g.n[0] + 2 * g.h[0] > (1 << 30) || g.n[1] + 2 * g.h[1] > (1 << 30)) return false;
-    *max_fused = 1;
-    *default_fused = 1;
+    *max_fused = 2;
+    *default_fused = 2;
     return true;
 }
 
@@ -231,8 +415,45 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     return Status::Ok();
 }
 
+template <typename T, bool EXACT>
+Status launch2(const LaunchCtx& c, const void* in, void* out) {
+    const Geo& g = *c.g;
+    CUtensorMap map;
+    Status s = make_tmap_3d<T>(g, in, BXW<T>, BY, &map);
+    if (!s.ok()) return s;
+    BoxArgs<T> a;
+    a.n0 = (int)g.n[0];
+    a.n1 = (int)g.n[1];
+    a.n2 = (int)g.n[2];
+    a.tiles_x = (int)((g.n[2] + TX2<T> - 1) / TX2<T>);
+    a.tiles_y = (int)((g.n[1] + TY2 - 1) / TY2);
+    a.h0 = (int)g.h[0];
+    a.h1 = (int)g.h[1];
+    a.off2 = (int)g.off2;
+    a.pitch0 = g.pitch[0];
+    a.pitch1 = g.pitch[1];
+    a.origin = g.origin;
+    for (int q = 0; q < 27; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
+    constexpr int bytes = smem2_bytes<T>();
+    int per_sm = 1, nsm = 148;
+    s = occupancy(box3d_tb2_kernel<T, EXACT>, NT, bytes, &per_sm, &nsm);
+    if (!s.ok()) return s;
+    const long long tiles = (long long)a.tiles_x * a.tiles_y;
+    a.chunk = pick_chunk(g.n[0], tiles, (long long)nsm * per_sm, 4, 32);
+    const long long nchunks = (g.n[0] + a.chunk - 1) / a.chunk;
+    box3d_tb2_kernel<T, EXACT><<<(unsigned)(tiles * nchunks), NT, bytes, c.stream>>>(
+        static_cast<T*>(out), map, a);
+    TSR_CUDA_TRY(cudaGetLastError());
+    return Status::Ok();
+}
+
 Status run(const LaunchCtx& c, const void* in, void* out, int k) {
-    if (k != 1) return Status::Err(TSR_EUNSUPPORTED, "box3d fuses one step per pass");
+    if (k == 2) {
+        if (c.g->dtype == TSR_F64)
+            return c.exact ? launch2<double, true>(c, in, out) : launch2<double, false>(c, in, out);
+        return c.exact ? launch2<float, true>(c, in, out) : launch2<float, false>(c, in, out);
+    }
+    if (k != 1) return Status::Err(TSR_EUNSUPPORTED, "box3d fuses one or two steps per pass");
     if (c.g->dtype == TSR_F64)
         return c.exact ? launch<double, true>(c, in, out) : launch<double, false>(c, in, out);
     return c.exact ? launch<float, true>(c, in, out) : launch<float, false>(c, in, out);

@@ -110,18 +110,22 @@ def test_generic_engine_bitwise(ts, orc, name):
     assert both_buffers_equal(a, b)
 
 
+@pytest.mark.parametrize("fused", [1, 2])
 @pytest.mark.parametrize("dt", ["f64", "f32"])
-def test_box27_planesum_bitwise(ts, orc, dt):
-    """box3d engine: per-plane partial sums keep the oracle's tap order;
-    tiles cut by the grid edge, chunked a0, halo wider than r."""
+def test_box27_planesum_bitwise(ts, orc, dt, fused):
+    """box3d engine (k=1 and the k=2 two-level plane-sum pipeline): per-plane
+    partial sums keep the oracle's tap order; tiles cut by the grid edge,
+    chunked a0, halo wider than r, non-zero Dirichlet halo."""
     k = ts.find_benchmark("Box-3D27P").kernel
-    for extent, halo, steps in [([11, 19, 23], [1, 1, 1], 4), ([70, 45, 150], [2, 1, 3], 3),
-                                ([3, 3, 3], [1, 1, 1], 2)]:
+    for extent, halo, steps in [([11, 19, 23], [1, 1, 1], 4), ([70, 45, 150], [2, 1, 3], 5),
+                                ([3, 3, 3], [1, 1, 1], 2), ([40, 66, 130], [1, 1, 1], 3)]:
         a = random_grid(ts, orc, extent, halo, sum(extent), dt)
+        a.padded(0)[0] = 2.5  # a non-zero halo plane in both buffers
+        a.padded(1)[0] = 2.5
         b = a.copy()
-        st = ts.run_gpu(a, k, steps, engine="tuned")
+        st = ts.run_gpu(a, k, steps, engine="tuned", fused_steps=fused)
         orc.naive_run(b, k, steps)
-        assert st.engine == "tuned"
+        assert st.engine == "tuned" and st.fused_steps == fused
         assert both_buffers_equal(a, b), extent
         assert halos_equal(a, b)
 
