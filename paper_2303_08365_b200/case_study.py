@@ -1,0 +1,182 @@
+"""Thermal-diffusion case study (proj/include/tessera/case_study.hpp,
+proj/src/case_study.cpp:21-290) on the B200 path.
+
+A square plate with a Gaussian hot spot (peak 100 C) over a 20 C Dirichlet
+rim, explicit 5-point heat scheme (mu = 0.23), advanced in FP64 and, as a
+precision twin, in FP32; at checkpoints the FP32 field is compared with the
+FP64 one (Table-5-style exceedance table).  Both grids stay in HBM for the
+whole run; only the centre cell is read back per sample and whole fields
+only at checkpoints.  Desk scale is the reference's 480 x 480, 9500 steps;
+``apply_full_scale`` is the paper's 9600 x 9600, 3.8e6 steps (PAPER Table 4).
+
+The FP32 twin runs on the GPU in exact mode, which is bitwise the
+reference's CPU ``naive_run<float>``, so the error tables are the ones the
+reference would print.
+"""
+from __future__ import annotations
+
+import math
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from .device import DeviceGrid
+from .grid import Grid, GridF, dump_grid
+from .kernel import heat_coefficients
+
+
+@dataclass
+class ErrorTable:
+    """case_study.hpp:16-21."""
+    abs_thresholds: tuple = (0.1, 0.5, 1.0)
+    rel_thresholds: tuple = (0.01, 0.03, 0.05)
+    abs_exceed_pct: list = field(default_factory=lambda: [0.0, 0.0, 0.0])
+    rel_exceed_pct: list = field(default_factory=lambda: [0.0, 0.0, 0.0])
+
+
+def compare_precision(fp64: Grid, other, abs_thresholds=(0.1, 0.5, 1.0),
+                      rel_thresholds=(0.01, 0.03, 0.05)) -> ErrorTable:
+    """Share of interior points whose |other - fp64| (and relative deviation
+    with a 1e-12 floor) exceeds each threshold (case_study.cpp:21-47)."""
+    if other.dims != fp64.dims:
+        raise ValueError("grid dimensionality mismatch")
+    if other.extent != fp64.extent:
+        raise ValueError("grid extent mismatch")
+    r = fp64.interior_view(fp64.parity).astype(np.float64)
+    o = other.interior_view(other.parity).astype(np.float64)
+    d = np.abs(o - r)
+    rel = d / np.maximum(np.abs(r), 1e-12)
+    t = ErrorTable(tuple(abs_thresholds), tuple(rel_thresholds))
+    n = r.size
+    t.abs_exceed_pct = [100.0 * float(np.count_nonzero(d > a)) / n for a in abs_thresholds]
+    t.rel_exceed_pct = [100.0 * float(np.count_nonzero(rel > a)) / n for a in rel_thresholds]
+    return t
+
+
+@dataclass
+class CaseStudyConfig:
+    """case_study.hpp:31-45 (path is always the GPU here)."""
+    plate_side_mm: float = 15.0
+    mu: float = 0.23
+    extent: int = 480
+    steps: int = 9500
+    peak_celsius: float = 100.0
+    ambient_celsius: float = 20.0
+    sigma_cells: float = 0.0  # 0 -> extent / 8
+    checkpoints: list = field(default_factory=lambda: [1000, 5000, 9500])
+    sample_every: int = 25
+    fused_steps: int = 0      # 0 = engine default
+    mode: str = "exact"
+
+
+def apply_full_scale(cfg: CaseStudyConfig) -> None:
+    """case_study.cpp:118-125: 9600 x 9600, 3.8e6 steps, checkpoint at the end."""
+    cfg.extent = 9600
+    cfg.steps = 3_800_000
+    cfg.checkpoints = [cfg.steps]
+    cfg.sample_every = 10_000
+
+
+def _init(grid, cfg: CaseStudyConfig, sigma: float) -> None:
+    """Interior Gaussian over a cold-ambient Dirichlet rim (case_study.cpp:193-207)."""
+    n = cfg.extent
+    c0 = (n - 1) / 2.0
+    idx = np.arange(n, dtype=np.float64) - c0
+    r2 = idx[:, None] ** 2 + idx[None, :] ** 2
+    field_ = cfg.ambient_celsius + (cfg.peak_celsius - cfg.ambient_celsius) * np.exp(
+        -r2 / (2.0 * sigma * sigma))
+    grid.fill(cfg.ambient_celsius)
+    for w in (0, 1):
+        grid.interior_view(w)[...] = field_.astype(grid.dtype)
+
+
+def case_study_heat(cfg: CaseStudyConfig, out_dir: str | None = None, device=None) -> dict:
+    """Runs the study; writes center_series.csv, error_table.csv,
+    metadata.txt and final.ttrs into `out_dir` when given."""
+    import torch
+    if cfg.extent < 16:
+        raise ValueError("plate extent too small")
+    if cfg.steps < 0:
+        raise ValueError("negative step count")
+    for c in cfg.checkpoints:
+        if c > cfg.steps:
+            raise ValueError("checkpoint beyond the final step")
+        if c % cfg.sample_every != 0 and c != cfg.steps:
+            raise ValueError("checkpoint must fall on the sampling stride")
+    kernel = heat_coefficients(cfg.mu)
+    sigma = cfg.sigma_cells if cfg.sigma_cells > 0 else cfg.extent / 8.0
+    n = cfg.extent
+    fp64 = Grid([n, n], [1, 1])
+    fp32 = GridF([n, n], [1, 1])
+    _init(fp64, cfg, sigma)
+    _init(fp32, cfg, sigma)
+    dev = torch.device(device if device is not None else "cuda")
+    d64 = DeviceGrid(fp64, dev)
+    d32 = DeviceGrid(fp32, dev)
+    center = n // 2
+
+    def center_of(dg: DeviceGrid) -> float:
+        e = dg.layout.origin + center * dg.layout.pitch[0] + center
+        return float(dg.buf[dg.cur][e].item())
+
+    res = {"series_steps": [0], "center_series": [float(fp64.at(center, center))],
+           "checkpoint_steps": [], "checkpoint_errors": [], "artifacts": []}
+    t64 = t32 = 0.0
+    done = 0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    while done < cfg.steps:
+        chunk = min(cfg.sample_every, cfg.steps - done)
+        ev[0].record()
+        d64.advance(kernel, chunk, fused_steps=cfg.fused_steps, mode=cfg.mode)
+        ev[1].record()
+        d32.advance(kernel, chunk, fused_steps=cfg.fused_steps, mode=cfg.mode)
+        ev[2].record()
+        done += chunk
+        res["series_steps"].append(done)
+        res["center_series"].append(center_of(d64))  # synchronises
+        t64 += ev[0].elapsed_time(ev[1]) / 1e3
+        t32 += ev[1].elapsed_time(ev[2]) / 1e3
+        if done in cfg.checkpoints:
+            h64, h32 = Grid([n, n], [1, 1]), GridF([n, n], [1, 1])
+            _init(h64, cfg, sigma)
+            _init(h32, cfg, sigma)
+            d64.download(h64)
+            d32.download(h32)
+            d64.steps_done = d32.steps_done = 0  # keep stepping from the device state
+            res["checkpoint_steps"].append(done)
+            res["checkpoint_errors"].append(compare_precision(h64, h32))
+            fp64, fp32 = h64, h32
+    res["final_center"] = res["center_series"][-1]
+    pts = n * n * cfg.steps
+    res["fp64_device_s"] = t64
+    res["fp32_device_s"] = t32
+    res["fp64_gstencil_s"] = pts / t64 / 1e9 if t64 > 0 else 0.0
+    res["fp32_gstencil_s"] = pts / t32 / 1e9 if t32 > 0 else 0.0
+    if out_dir:
+        os.makedirs(out_dir, exist_ok=True)
+        with open(os.path.join(out_dir, "center_series.csv"), "w") as f:
+            f.write("step,center_celsius\n")
+            for s, c in zip(res["series_steps"], res["center_series"]):
+                f.write(f"{s},{c!r}\n")
+        with open(os.path.join(out_dir, "error_table.csv"), "w") as f:
+            f.write("step,abs_gt_0.1,abs_gt_0.5,abs_gt_1.0,rel_gt_1pct,rel_gt_3pct,rel_gt_5pct\n")
+            for s, t in zip(res["checkpoint_steps"], res["checkpoint_errors"]):
+                f.write(f"{s}," + ",".join(f"{v:.4f}" for v in t.abs_exceed_pct + t.rel_exceed_pct)
+                        + "\n")
+        if res["checkpoint_steps"] and res["checkpoint_steps"][-1] == cfg.steps:
+            dump_grid(os.path.join(out_dir, "final.ttrs"), fp64)
+            res["artifacts"].append(os.path.join(out_dir, "final.ttrs"))
+        with open(os.path.join(out_dir, "metadata.txt"), "w") as f:
+            f.write(f"extent = {n}\nsteps = {cfg.steps}\nmu = {cfg.mu}\nsigma_cells = {sigma}\n"
+                    f"peak_celsius = {cfg.peak_celsius}\nambient_celsius = {cfg.ambient_celsius}\n"
+                    f"final_center_celsius = {res['final_center']!r}\n"
+                    f"fp64_device_s = {t64:.3f}\nfp32_device_s = {t32:.3f}\n"
+                    f"fp64_gstencil_s = {res['fp64_gstencil_s']:.2f}\n"
+                    f"fp32_gstencil_s = {res['fp32_gstencil_s']:.2f}\n"
+                    f"mode = {cfg.mode}\n")
+        res["artifacts"] += [os.path.join(out_dir, x) for x in
+                             ("center_series.csv", "error_table.csv", "metadata.txt")]
+    return res
