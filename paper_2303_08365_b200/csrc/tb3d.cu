@@ -41,7 +41,7 @@ constexpr int NLX = R1X / VX;  // 32 lanes
 constexpr int NLY = R1Y / VY;  // 16 warps
 constexpr int NT = NLX * NLY;  // 512 threads
 constexpr int BY0 = R1Y + 2;   // TMA box height: 1 extra row per side
-constexpr int STAGES = 4;
+constexpr int STAGES = 5;  // planes t-2 .. t+2 of the level-0 ring
 constexpr int LEVY = R1Y + 2;  // level buffer rows (1 padding row per side)
 
 template <typename T>
@@ -77,9 +77,10 @@ template <typename T>
 constexpr int lev_bytes() {
     return (LEVY * R1X * (int)sizeof(T) + 127) / 128 * 128;
 }
+constexpr int NLEV = 3;  // level-l planes are read two steps after they are written
 template <typename T, int K>
 constexpr int smem_bytes() {
-    return STAGES * slot_bytes<T>() + 2 * (K - 1) * lev_bytes<T>() + STAGES * 8;
+    return STAGES * slot_bytes<T>() + NLEV * (K - 1) * lev_bytes<T>() + STAGES * 8;
 }
 
 template <typename T>
@@ -113,10 +114,15 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
     return madd<EXACT>(acc, w[6], next);
 }
 
-// One plane step of the wavefront (iteration `it`, PH = it % 3).  Register
-// history per level l: Hs[l][s] holds the level-l value of plane q with
-// (q - t_begin) % 3 == s, so the three-plane window rotates by renaming and
-// the time loop (unrolled by 3) needs no register moves.
+// One step of the wavefront (iteration `it`, PH = it % 3).  Level l works on
+// plane t - 2l: two planes behind level l-1, so every input of every level
+// was produced in an earlier step and the K levels' dependency chains are
+// independent within a step.  Levels run in descending order: level l+1
+// consumes the oldest plane of level l's three-plane register window before
+// level l overwrites it.  Hs[l][s] holds the level-l value of plane q with
+// (q - t_begin) % 3 == s, so the window rotates by renaming (loop unrolled
+// by 3).  a1-neighbour rows of other warps are read two steps after they
+// were written (3-deep SMEM buffers, one __syncthreads per step).
 template <typename T, int K, bool EXACT, int PH, bool SEL>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
                                           uint64_t* bar, int it, int t_begin, int i0, int i1,
@@ -128,32 +134,22 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
     constexpr int LEV = lev_bytes<T>() / (int)sizeof(T);
     constexpr int BX = BX0<T>, PL = PADL<T>;
     const int t = t_begin + it;
-    const int slot = it % STAGES;
-    mbar_wait(&bar[slot], (it / STAGES) & 1);
-    const T* P0 = ring + slot * SLOT;                         // level 0, plane t
-    const T* Pm = ring + ((it + STAGES - 1) % STAGES) * SLOT;  // level 0, plane t-1
-
-    // Level 0: plane t of the owned columns.
-#pragma unroll
-    for (int cy = 0; cy < VY; ++cy) {
-        const P2 v = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
-        Hs[0][PH][cy][0] = v.x;
-        Hs[0][PH][cy][1] = v.y;
-    }
 
 #pragma unroll
-    for (int l = 1; l <= K; ++l) {
-        const int p = t - l;  // plane level l produces now
-        const int sP = ((PH - l - 1) % 3 + 3) % 3;  // slot of plane p-1
-        const int sC = ((PH - l) % 3 + 3) % 3;      // slot of plane p
-        const int sN = ((PH - l + 1) % 3 + 3) % 3;  // slot of plane p+1
-        // a1-neighbour rows y-1 and y+VY of level l-1 at plane p.
+    for (int l = K; l >= 1; --l) {
+        const int p = t - 2 * l;                          // plane level l produces now
+        const int sP = ((PH - 2 * l - 1) % 3 + 3) % 3;    // slot of plane p-1
+        const int sC = ((PH - 2 * l) % 3 + 3) % 3;        // slot of plane p
+        const int sN = ((PH - 2 * l + 1) % 3 + 3) % 3;    // slot of plane p+1
+        // a1-neighbour rows y-1 and y+VY of level l-1 at plane p
         P2 u, d;
+        const T* Pm = nullptr;
         if (l == 1) {
+            Pm = ring + ((it - 2 + 2 * STAGES) % STAGES) * SLOT;  // level 0, plane t-2
             u = *reinterpret_cast<const P2*>(Pm + (y) * BX + x + PL);
             d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX + x + PL);
         } else {
-            const T* L = lev + ((l - 2) * 2 + (p & 1)) * LEV;
+            const T* L = lev + ((l - 2) * NLEV + sC) * LEV;
             u = *reinterpret_cast<const P2*>(L + (y) * R1X + x);
             d = *reinterpret_cast<const P2*>(L + (y + VY + 1) * R1X + x);
         }
@@ -177,7 +173,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                                          Hs[l - 1][sN][cy][1]);
         }
         // Dirichlet: cells outside the interior keep their level-0 value
-        // (only the SEL instantiation, used for edge tiles / edge planes).
+        // (only the SEL instantiation, used for edge warps / edge planes).
         if constexpr (SEL) {
             const bool pint = p >= 0 && p < a.n0;
 #pragma unroll
@@ -187,7 +183,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                     if (!(pint && cint[cy][cx])) res[cy][cx] = Hs[l - 1][sC][cy][cx];
         }
         if (l < K) {
-            T* L = lev + ((l - 1) * 2 + (p & 1)) * LEV;
+            T* L = lev + ((l - 1) * NLEV + sC) * LEV;
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy) {
                 P2 v;
@@ -204,9 +200,18 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
             for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx)
-                    if (cout[cy][cx])
-                        o[cy * a.pitch1 + cx] = EXACT ? res[cy][cx] + T(0) : res[cy][cx];
+                    if (cout[cy][cx]) o[cy * a.pitch1 + cx] = fix_zero<EXACT>(res[cy][cx]);
         }
+    }
+    // Level 0 last: plane t into the window slot level 1 has just consumed.
+    const int slot = it % STAGES;
+    mbar_wait(&bar[slot], (it / STAGES) & 1);
+    const T* P0 = ring + slot * SLOT;
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy) {
+        const P2 v = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
+        Hs[0][PH][cy][0] = v.x;
+        Hs[0][PH][cy][1] = v.y;
     }
 }
 
@@ -218,8 +223,8 @@ __global__ void __launch_bounds__(NT, 1)
     constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
     T* ring = reinterpret_cast<T*>(smem);
     T* lev = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T>());
-    uint64_t* bar =
-        reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>() + 2 * (K - 1) * lev_bytes<T>());
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>() +
+                                                NLEV * (K - 1) * lev_bytes<T>());
 
     const int tid = threadIdx.x;
     const int lx = tid & 31, ly = tid >> 5;
@@ -233,8 +238,10 @@ __global__ void __launch_bounds__(NT, 1)
     const int gy = by * TY - (K - 1);  // global a1 of region-1 row 0
     const int i0 = bz * a.chunk;
     const int i1 = min(i0 + a.chunk, a.n0);
-    const int t_begin = i0 - K, t_end = i1 + K;
+    // level-0 planes i0-K .. i1+K-1; level K finishes plane i1-1 at step i1-1+2K
+    const int t_begin = i0 - K, t_end = i1 + 2 * K;
     const int niter = t_end - t_begin;
+    const int nload = i1 - i0 + 2 * K;  // level-0 planes actually needed
 
     // Columns owned: region-1 (y, x) = (VY*ly + cy, VX*lx + cx).
     const int x = VX * lx, y = VY * ly;
@@ -257,12 +264,16 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     constexpr unsigned kBoxBytes = BX0<T> * BY0 * sizeof(T);
     const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned box start
+    // plane index j (0-based from t_begin) is loaded at most once; steps past
+    // the last needed plane load planes beyond the chunk (zero-filled or real
+    // data, never stored)
     if (tid == 0) {
         for (int s = 0; s < STAGES && s < niter; ++s) {
             mbar_expect_tx(&bar[s], kBoxBytes);
             tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + s);
         }
     }
+    (void)nload;
 
     T Hs[K][3][VY][VX];
 #pragma unroll
@@ -276,34 +287,35 @@ __global__ void __launch_bounds__(NT, 1)
 
     auto after = [&](int it) {
         __syncthreads();
-        // Plane t-1's slot is free: refill it with plane t-1+STAGES.
-        if (tid == 0 && it >= 1 && it - 1 + STAGES < niter) {
-            const int s = (it - 1) % STAGES;
+        // Plane t-2 was last read in this step (level-1 neighbours): its slot
+        // takes plane t-2+STAGES.
+        if (tid == 0 && it >= 2 && it - 2 + STAGES < niter) {
+            const int s = (it - 2) % STAGES;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&bar[s], kBoxBytes);
             tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1,
-                           a.h0 + t_begin + it - 1 + STAGES);
+                        a.h0 + t_begin + it - 2 + STAGES);
         }
     };
-    // Planes t-K..t-1 all interior and no column of this warp on the a1/a2
-    // boundary: no Dirichlet selects needed in this step (warp-uniform).
     bool mine = true;
 #pragma unroll
     for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
         for (int cx = 0; cx < VX; ++cx) mine &= cint[cy][cx];
     const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in this warp
+    // Planes t-2K..t-2 all interior and no column of this warp on the a1/a2
+    // boundary: no Dirichlet selects needed in this step (warp-uniform).
     auto clear = [&](int it) {
         const int t = t_begin + it;
-        return warp_int && t - K >= 0 && t - 1 < a.n0;
+        return warp_int && t - 2 * K >= 0 && t - 2 < a.n0;
     };
 #define TB3D_STEP(PH, IT)                                                                    \
     if (clear(IT))                                                                           \
         tb3d_step<T, K, EXACT, PH, false>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x, \
-                                          y, gx, gy, cint, cout, Hs);              \
+                                          y, gx, gy, cint, cout, Hs);                        \
     else                                                                                     \
         tb3d_step<T, K, EXACT, PH, true>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x,  \
-                                         y, gx, gy, cint, cout, Hs);               \
+                                         y, gx, gy, cint, cout, Hs);                         \
     after(IT);
     for (int it = 0; it < niter; it += 3) {
         TB3D_STEP(0, it)
@@ -317,7 +329,7 @@ __global__ void __launch_bounds__(NT, 1)
 #undef TB3D_STEP
 }
 
-constexpr int kMaxK = 4;
+constexpr int kMaxK = 3;  // k = 4 needs more SMEM than the 5-stage ring leaves
 
 bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
     if (t.dims != 3 || t.shape != TSR_STAR || t.radius != 1 || t.ntaps != 7) return false;
@@ -370,8 +382,7 @@ Status launch_m(const LaunchCtx& c, const void* in, void* out, int k) {
         case 1: return launch_k<T, 1, EXACT>(c, in, out);
         case 2: return launch_k<T, 2, EXACT>(c, in, out);
         case 3: return launch_k<T, 3, EXACT>(c, in, out);
-        case 4: return launch_k<T, 4, EXACT>(c, in, out);
-        default: return Status::Err(TSR_EUNSUPPORTED, "tb3d: fused steps must be 1..4");
+        default: return Status::Err(TSR_EUNSUPPORTED, "tb3d: fused steps must be 1..3");
     }
 }
 

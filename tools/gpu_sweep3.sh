@@ -8,4 +8,4 @@ run() { timeout 300 env $1 python bench.py --no-cpu --no-e2e ${@:2} 2>>gpurun_ou
 try:
  d=json.loads(sys.stdin.read()); print('$1 ${*:2}', d['value'], d['roofline']['frac'], d['config']['engine'], d['config']['fused_steps'], d['ms_per_step'], d['clocks']['sm_mhz'])
 except Exception: print('$1 ${*:2} FAILED')"; }
-for k in 1 2 3 4; do run X=1 --fused $k; run X=1 --fused $k --mode fast; done
+for k in 1 2 3; do run X=1 --fused $k; run X=1 --fused $k --mode fast; done
