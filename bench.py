@@ -45,7 +45,9 @@ CONFIGS = {
                workload="C3: 3D heat 7-point star fp64, 512^3 per GPU, 1000 timesteps",
                ref_tile=[20, 20, 20], ref_tb=10),
     "c4": dict(bench="Box-3D27P", extent=[1024, 1024, 1024], dtype="f32", steps=100, fused=0,
-               mode="fast", workload="C4: 3D 27-point box fp32, 1024^3, fast (FMA) mode",
+               mode="fast", strong=True,
+               workload="C4: 3D 27-point box fp32, 1024^3 global, slab-partitioned over N GPUs "
+                        "(strong scaling), fast (FMA) mode",
                ref_tile=None, ref_tb=None),
     "c5": dict(bench="Heat-3D", extent=[1024, 1024, 1024], dtype="f64", steps=100, fused=0,
                mode="exact", workload="C5: 3D heat 7-point fp64, 1024^3 per GPU (weak scaling)",
@@ -248,7 +250,10 @@ def main():
     fused_req = cfg["fused"] if args.fused is None else args.fused
     k = ts.find_benchmark(cfg["bench"]).kernel
     esize = 8 if cfg["dtype"] == "f64" else 4
+    strong = cfg.get("strong", False)
     per_gpu = list(cfg["extent"])
+    if strong:  # fixed global grid split along axis 0
+        per_gpu[0] = cfg["extent"][0] // world
     points_per_gpu = 1
     for e in per_gpu:
         points_per_gpu *= e
@@ -266,7 +271,7 @@ def main():
     else:
         from paper_2303_08365_b200.partition import SlabRunner, plan_slabs
         kfused_guess = fused_req if fused_req else 1
-        glob = [per_gpu[0] * world] + per_gpu[1:]
+        glob = list(cfg["extent"]) if strong else [per_gpu[0] * world] + per_gpu[1:]
         plan = plan_slabs(glob, k.radius, kfused_guess, world, rank)
         runner = SlabRunner.synthetic(ts, k, plan, cfg["dtype"], dev, seed=1 + rank,
                                       fused_steps=fused_req, mode=mode)
@@ -308,7 +313,9 @@ def main():
         dist.all_reduce(lt)
         launches = int(lt[0])
 
-    total_points = points_per_gpu * world
+    total_points = 1
+    for e in (cfg["extent"] if strong else [per_gpu[0] * world] + per_gpu[1:]):
+        total_points *= e
     value = total_points * args.steps / (elapsed_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
     # Algorithmic bytes of one fused launch on one GPU: 2*sizeof(T) per stencil
@@ -351,12 +358,13 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": round(elapsed_ms / args.steps, 5),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
         "dtype": cfg["dtype"],
         "data": "synthetic: fill_random(seed=1) U[0,1) interior, zero Dirichlet halo",
         "config": {"workload": cfg["workload"], "extent_per_gpu": per_gpu,
-                   "global_extent": [per_gpu[0] * world] + per_gpu[1:],
+                   "global_extent": (list(cfg["extent"]) if strong
+                                     else [per_gpu[0] * world] + per_gpu[1:]),
                    "kernel": cfg["bench"], "mode": mode, "fused_steps": kfused,
                    "engine": {1: "generic", 2: "tuned"}.get(engine, str(engine)),
                    "parallelism": f"slab{world}" if world > 1 else "single",
