@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--mode", default=None, choices=["exact", "fast"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="N>1: exchange, then the whole slab (no interior/seam split)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 path with ranks sharing one GPU")
     args = ap.parse_args()
@@ -274,7 +276,8 @@ def main():
         glob = list(cfg["extent"]) if strong else [per_gpu[0] * world] + per_gpu[1:]
         plan = plan_slabs(glob, k.radius, kfused_guess, world, rank)
         runner = SlabRunner.synthetic(ts, k, plan, cfg["dtype"], dev, seed=1 + rank,
-                                      fused_steps=fused_req, mode=mode)
+                                      fused_steps=fused_req, mode=mode,
+                                      overlap=not args.no_overlap)
         kfused = runner.fused_steps
         engine = 2
         advance = runner.advance

@@ -142,6 +142,17 @@ int tsr_copy_halo(const tsr_grid* g, const tsr_layout* l, const void* src, void*
 int tsr_advance(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, void* dev0,
                 void* dev1, int32_t* cur, int64_t steps, int32_t keep_previous,
                 const tsr_opts* opts, void* stream, tsr_stats* stats);
+/* One fused pass of `steps` (1..k of tsr_query_plan) time steps from `in` to
+ * `out` that stores only the planes [lo, hi) of the grid's axis 0 (interior
+ * coordinates); every other cell of `out` is left untouched.  Inputs are read
+ * from all planes of `in` the dependency cone needs (r*steps planes beyond
+ * the range, halo included).  This is HaloWorker::step_range
+ * (proj/src/scheduler.cpp:352-356) for a slab decomposition: the interior
+ * planes of a slab are launched while its ghost planes are still in flight
+ * and the seam planes after they land. */
+int tsr_sweep_range(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, const void* in,
+                    void* out, int64_t lo, int64_t hi, int32_t steps, const tsr_opts* opts,
+                    void* stream);
 /* Reports the engine (tsr_engine) and fused step count k tsr_advance /
  * tsr_run would use for this kernel, grid and opts (no device work). */
 int tsr_query_plan(const tsr_kernel* k, const tsr_grid* g, const tsr_opts* opts,

@@ -25,7 +25,7 @@ MODES = {"exact": TSR_EXACT, "fast": TSR_FAST}
 EXPORTED = (
     "tsr_abi_version", "tsr_last_error", "tsr_release_cache", "tsr_check_kernel",
     "tsr_fill_random", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
-    "tsr_copy_halo", "tsr_advance", "tsr_query_plan", "tsr_apply_box",
+    "tsr_copy_halo", "tsr_advance", "tsr_query_plan", "tsr_apply_box", "tsr_sweep_range",
 )
 
 
@@ -122,6 +122,9 @@ def lib() -> ctypes.CDLL:
                                      p(ctypes.c_int32)]
         L.tsr_apply_box.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrLayout), c_void_p, c_void_p,
                                     p(ctypes.c_int64), p(ctypes.c_int64), p(TsrOpts), c_void_p]
+        L.tsr_sweep_range.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrLayout), c_void_p,
+                                      c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                      p(TsrOpts), c_void_p]
         for name in EXPORTED:
             if name not in ("tsr_abi_version", "tsr_last_error"):
                 getattr(L, name).restype = ctypes.c_int

@@ -262,8 +262,12 @@ Status plan_for(const Geo& g, const TapSet& t, const tsr_opts& o, Plan& p) {
 
 Status sweep(const LaunchCtx& c, const Plan& p, const void* in, void* out, int k) {
     if (p.engine) return p.engine->run(c, in, out, k);
-    const int64_t lo[3] = {0, 0, 0};
-    const int64_t hi[3] = {c.g->n[0], c.g->n[1], c.g->n[2]};
+    int64_t lo[3] = {0, 0, 0};
+    int64_t hi[3] = {c.g->n[0], c.g->n[1], c.g->n[2]};
+    const int s = 3 - c.g->dims;
+    lo[s] = c.range_lo();
+    hi[s] = c.range_hi();
+    if (hi[s] <= lo[s]) return Status::Ok();
     return generic_sweep(c, in, out, lo, hi);
 }
 
@@ -560,6 +564,33 @@ int tsr_advance(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, voi
                 static_cast<cudaStream_t>(stream), stats);
     if (s.ok()) *cur = c;
     return report(s);
+}
+
+int tsr_sweep_range(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, const void* in,
+                    void* out, int64_t lo, int64_t hi, int32_t steps, const tsr_opts* opts,
+                    void* stream) {
+    if (!k || !g || !in || !out) return report(Status::Err(TSR_EINVAL, "null argument"));
+    if (in == out) return report(Status::Err(TSR_EINVAL, "in and out must be distinct buffers"));
+    Geo geo;
+    Status s = make_geo(*g, geo);
+    if (s.ok()) s = check_layout(geo, l);
+    TapSet t;
+    if (s.ok()) s = make_taps(*k, t);
+    if (s.ok()) s = check_applicable(geo, t);
+    if (!s.ok()) return report(s);
+    const int64_t n = geo.n[3 - geo.dims];
+    if (lo < 0 || hi > n || lo > hi)
+        return report(Status::Err(TSR_EINVAL, "plane range outside the grid's axis 0"));
+    const tsr_opts o = opts_or_default(opts);
+    Plan p;
+    s = plan_for(geo, t, o, p);
+    if (!s.ok()) return report(s);
+    if (steps < 1 || steps > p.k)
+        return report(Status::Err(TSR_EINVAL, "steps must be 1..k of the engine plan"));
+    LaunchCtx c{&geo, &t, o.mode != TSR_FAST, static_cast<cudaStream_t>(stream)};
+    c.lo0 = lo;
+    c.hi0 = hi;
+    return report(sweep(c, p, in, out, steps));
 }
 
 int tsr_query_plan(const tsr_kernel* k, const tsr_grid* g, const tsr_opts* opts,

@@ -51,6 +51,7 @@ template <typename T>
 struct BoxArgs {
     int n0, n1, n2;
     int tiles_x, tiles_y, chunk;
+    int lo0, hi0;  // output planes [lo0, hi0) of a0
     int h0, h1, off2;
     long long pitch0, pitch1, origin;
     T w[27];
@@ -108,8 +109,8 @@ __global__ void __launch_bounds__(NT) box3d_kernel(T* __restrict__ out,
     const int by = (tile / a.tiles_x) % a.tiles_y;
     const int bz = tile / (a.tiles_x * a.tiles_y);
     const int gx = bx * OX, gy = by * OY;  // interior coords of the tile origin
-    const int i0 = bz * a.chunk;
-    const int i1 = min(i0 + a.chunk, a.n0);
+    const int i0 = a.lo0 + bz * a.chunk;
+    const int i1 = min(i0 + a.chunk, a.hi0);
     // planes i0-1 .. i1 feed outputs i0 .. i1-1
     const int t_begin = i0 - 1, niter = i1 - i0 + 2;
     const int x = VX * lx, y = VY * ly;
@@ -241,8 +242,8 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
     const int bz = tile / (a.tiles_x * a.tiles_y);
     constexpr int HX = HX2<T>, TX = TX2<T>, BW = BWP<T>;
     const int gx = bx * TX - HX, gy = by * TY2 - 1;  // global coords of L1 cell (0, 0)
-    const int i0 = bz * a.chunk;
-    const int i1 = min(i0 + a.chunk, a.n0);
+    const int i0 = a.lo0 + bz * a.chunk;
+    const int i1 = min(i0 + a.chunk, a.hi0);
     // level-0 planes i0-2 .. i1+1 feed level-2 outputs i0 .. i1-1
     const int t_begin = i0 - 2, niter = i1 - i0 + 4;
     const int x = VX * lx, y = VY * ly;
@@ -407,8 +408,12 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     s = occupancy(box3d_kernel<T, EXACT>, NT, bytes, &per_sm, &nsm);
     if (!s.ok()) return s;
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
-    a.chunk = pick_chunk(g.n[0], tiles, (long long)nsm * per_sm, 2, 32);
-    const long long nchunks = (g.n[0] + a.chunk - 1) / a.chunk;
+    a.lo0 = (int)c.range_lo();
+    a.hi0 = (int)c.range_hi();
+    if (a.hi0 <= a.lo0) return Status::Ok();
+    const int64_t span = a.hi0 - a.lo0;
+    a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 2, 32);
+    const long long nchunks = (span + a.chunk - 1) / a.chunk;
     box3d_kernel<T, EXACT><<<(unsigned)(tiles * nchunks), NT, bytes, c.stream>>>(
         static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());
@@ -439,8 +444,12 @@ Status launch2(const LaunchCtx& c, const void* in, void* out) {
     s = occupancy(box3d_tb2_kernel<T, EXACT>, NT, bytes, &per_sm, &nsm);
     if (!s.ok()) return s;
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
-    a.chunk = pick_chunk(g.n[0], tiles, (long long)nsm * per_sm, 4, 32);
-    const long long nchunks = (g.n[0] + a.chunk - 1) / a.chunk;
+    a.lo0 = (int)c.range_lo();
+    a.hi0 = (int)c.range_hi();
+    if (a.hi0 <= a.lo0) return Status::Ok();
+    const int64_t span = a.hi0 - a.lo0;
+    a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 4, 32);
+    const long long nchunks = (span + a.chunk - 1) / a.chunk;
     box3d_tb2_kernel<T, EXACT><<<(unsigned)(tiles * nchunks), NT, bytes, c.stream>>>(
         static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());

@@ -135,6 +135,15 @@ struct LaunchCtx {
     const TapSet* taps;
     bool exact;
     cudaStream_t stream;
+    // Output planes [lo0, hi0) along the grid's own axis 0 (normalised axis
+    // 3 - dims): the slab axis of a multi-GPU partition.  A fused pass still
+    // reads every input plane its dependency cone needs; only the stores are
+    // restricted, so interior and seam planes can be launched separately.
+    int64_t lo0 = 0;
+    int64_t hi0 = INT64_MAX;
+
+    int64_t range_lo() const { return lo0; }
+    int64_t range_hi() const { return std::min<int64_t>(hi0, g->n[3 - g->dims]); }
 };
 
 // One sweep over the normalised box [lo, hi) from `in` to `out` (apply_box).

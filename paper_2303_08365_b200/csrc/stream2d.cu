@@ -31,6 +31,7 @@ struct S2Args {
     int64_t origin;          // element index of interior (0,0)
     int64_t col_lo, col_hi;  // allocated column range relative to interior col 0
     int64_t chunk;           // output rows per warp
+    int64_t row_lo, row_hi;  // output rows [row_lo, row_hi) (the grid's axis 0)
     int64_t nstrips;
     int64_t wout;            // output columns per strip
     int64_t hl;              // left margin of the strip (>= R*K, vector aligned)
@@ -101,8 +102,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     if (gw >= a.total_warps) return;
     const int64_t strip = gw % a.nstrips;
     const int64_t chunk = gw / a.nstrips;
-    const int64_t rb = chunk * a.chunk;
-    const int64_t re = min(rb + a.chunk, a.rows);
+    const int64_t rb = a.row_lo + chunk * a.chunk;
+    const int64_t re = min(rb + a.chunk, a.row_hi);
     const int64_t ob = strip * a.wout;                 // first output column
     const int64_t oe = min(ob + a.wout, a.cols);       // output column end
     const int64_t c0 = ob - a.hl + (int64_t)lane * V;  // this lane's first column
@@ -274,8 +275,12 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     // Aim for ~16 resident warps per SM, chunks of >= 16*K*R rows.
     const int64_t target = 148 * 24;
     int64_t nchunks = std::max<int64_t>(1, target / a.nstrips);
-    a.chunk = std::max<int64_t>(16 * K * R, (a.rows + nchunks - 1) / nchunks);
-    nchunks = (a.rows + a.chunk - 1) / a.chunk;
+    a.row_lo = c.range_lo();
+    a.row_hi = c.range_hi();
+    if (a.row_hi <= a.row_lo) return Status::Ok();
+    const int64_t span = a.row_hi - a.row_lo;
+    a.chunk = std::max<int64_t>(16 * K * R, (span + nchunks - 1) / nchunks);
+    nchunks = (span + a.chunk - 1) / a.chunk;
     a.total_warps = nchunks * a.nstrips;
     for (int t = 0; t < c.taps->ntaps; ++t) a.w[t] = static_cast<T>(c.taps->w[t]);
     const unsigned blocks =

@@ -21,6 +21,7 @@ struct Star3Args {
     int64_t pitch0, pitch1;
     int64_t origin;
     int64_t chunk;  // a0 planes per CTA
+    int64_t lo0, hi0;  // output planes [lo0, hi0) of a0
     T w[7];
 };
 
@@ -30,8 +31,8 @@ __global__ void __launch_bounds__(kBX* kBY) star3d_r1_kernel(const T* __restrict
                                                             const __grid_constant__ Star3Args<T> a) {
     const int64_t k = blockIdx.x * (int64_t)kBX + threadIdx.x;
     const int64_t j = blockIdx.y * (int64_t)kBY + threadIdx.y;
-    const int64_t i0 = blockIdx.z * a.chunk;
-    const int64_t i1 = min(i0 + a.chunk, a.n0);
+    const int64_t i0 = a.lo0 + blockIdx.z * a.chunk;
+    const int64_t i1 = min(i0 + a.chunk, a.hi0);
     if (k >= a.n2 || j >= a.n1) return;
     int64_t p = a.origin + i0 * a.pitch0 + j * a.pitch1 + k;
     const int64_t P0 = a.pitch0, P1 = a.pitch1;
@@ -74,8 +75,12 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     const int64_t gx = (g.n[2] + kBX - 1) / kBX, gy = (g.n[1] + kBY - 1) / kBY;
     // Enough CTAs for ~8 resident per SM, but chunks of >= 32 planes.
     int64_t nz = std::max<int64_t>(1, (148 * 8 + gx * gy - 1) / (gx * gy));
-    a.chunk = std::max<int64_t>(32, (g.n[0] + nz - 1) / nz);
-    nz = (g.n[0] + a.chunk - 1) / a.chunk;
+    a.lo0 = c.range_lo();
+    a.hi0 = c.range_hi();
+    if (a.hi0 <= a.lo0) return Status::Ok();
+    const int64_t span = a.hi0 - a.lo0;
+    a.chunk = std::max<int64_t>(32, (span + nz - 1) / nz);
+    nz = (span + a.chunk - 1) / a.chunk;
     dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(nz));
     dim3 block(kBX, kBY);
     if (c.exact)

@@ -88,6 +88,7 @@ struct TbArgs {
     int n0, n1, n2;
     int tiles_x, tiles_y;
     int chunk;
+    int lo0, hi0;  // output planes [lo0, hi0) of a0
     int h0, h1, off2;
     long long pitch0, pitch1, origin;
     T w[7];
@@ -236,8 +237,8 @@ __global__ void __launch_bounds__(NT, 1)
     constexpr int PL = PADL<T>, HX = HXL<T, K>;
     const int gx = bx * TX - HX;       // global a2 of region-1 column 0
     const int gy = by * TY - (K - 1);  // global a1 of region-1 row 0
-    const int i0 = bz * a.chunk;
-    const int i1 = min(i0 + a.chunk, a.n0);
+    const int i0 = a.lo0 + bz * a.chunk;
+    const int i1 = min(i0 + a.chunk, a.hi0);
     // level-0 planes i0-K .. i1+K-1; level K finishes plane i1-1 at step i1-1+2K
     const int t_begin = i0 - K, t_end = i1 + 2 * K;
     const int niter = t_end - t_begin;
@@ -264,16 +265,18 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     constexpr unsigned kBoxBytes = BX0<T> * BY0 * sizeof(T);
     const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned box start
-    // plane index j (0-based from t_begin) is loaded at most once; steps past
-    // the last needed plane load planes beyond the chunk (zero-filled or real
-    // data, never stored)
+    // plane index j (0-based from t_begin) is loaded at most once; the steps
+    // that drain the wavefront past the last needed plane (i1+K-1) re-load
+    // that plane instead, so a launch never reads outside its dependency cone
+    // (a slab's interior range runs while its ghost planes are being written)
+    const int last_plane = a.h0 + t_begin + nload - 1;
     if (tid == 0) {
         for (int s = 0; s < STAGES && s < niter; ++s) {
             mbar_expect_tx(&bar[s], kBoxBytes);
-            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1, a.h0 + t_begin + s);
+            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1,
+                        min(a.h0 + t_begin + s, last_plane));
         }
     }
-    (void)nload;
 
     T Hs[K][3][VY][VX];
 #pragma unroll
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(NT, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&bar[s], kBoxBytes);
             tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1,
-                        a.h0 + t_begin + it - 2 + STAGES);
+                        min(a.h0 + t_begin + it - 2 + STAGES, last_plane));
         }
     };
     bool mine = true;
@@ -360,8 +363,11 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     if (!s.ok()) return s;
     // a0 chunks: whole waves of resident CTAs, >= 48 planes (the 2K-plane
     // wavefront fill is overhead)
-    const int best_chunk = pick_chunk(g.n[0], tiles, (long long)nsm * per_sm, 2 * K, 48);
-    a.chunk = best_chunk;
+    a.lo0 = (int)c.range_lo();
+    a.hi0 = (int)c.range_hi();
+    if (a.hi0 <= a.lo0) return Status::Ok();
+    const int64_t span = a.hi0 - a.lo0;
+    a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 2 * K, 48);
     a.h0 = (int)g.h[0];
     a.h1 = (int)g.h[1];
     a.off2 = (int)g.off2;
@@ -369,7 +375,7 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.pitch1 = g.pitch[1];
     a.origin = g.origin;
     for (int q = 0; q < 7; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
-    const long long nchunks = (g.n[0] + a.chunk - 1) / a.chunk;
+    const long long nchunks = (span + a.chunk - 1) / a.chunk;
     const unsigned grid = (unsigned)(tiles * nchunks);
     tb3d_kernel<T, K, EXACT><<<grid, NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());

@@ -90,6 +90,32 @@ class DeviceGrid:
         self.steps_done += int(steps)
         return st
 
+    def sweep_range(self, kernel: StencilKernel, lo: int, hi: int, steps: int, *,
+                    fused_steps: int = 0, mode: str = "exact", engine: str = "auto",
+                    stream=None) -> int:
+        """One fused pass of `steps` time steps from the current buffer into
+        the other one, storing only the planes [lo, hi) of axis 0
+        (tsr_sweep_range).  Does not flip the buffers: a slab round launches
+        its interior and seam ranges separately, then calls ``flip``.
+        Returns the number of kernels launched (0 for an empty range)."""
+        if hi <= lo:
+            return 0
+        L = _abi.lib()
+        opts = _abi.make_opts(fused_steps, mode, engine)
+        with self.torch.cuda.device(self.device):
+            _abi.check(L.tsr_sweep_range(ctypes.byref(kernel.c_struct()), ctypes.byref(self.desc),
+                                         ctypes.byref(self.layout), self.ptr(self.cur),
+                                         self.ptr(1 - self.cur), int(lo), int(hi), int(steps),
+                                         ctypes.byref(opts), self._stream(stream)))
+        return 1
+
+    def flip(self, steps: int) -> None:
+        """Makes the other buffer current after a round of `steps` steps
+        written by ``sweep_range`` calls."""
+        self.cur ^= 1
+        self.steps_done += int(steps)
+        self.prev_valid = steps == 1
+
     def download(self, grid: BasicGrid, stream=None) -> None:
         """Interior of the current buffer -> grid.buffer(final parity); the
         previous step (when kept) -> the other buffer; parity flipped by the

@@ -17,6 +17,13 @@ CPU+GPU ratio split is out of scope per the north star):
   batch_isend_irecv over NVLink/NVSwitch); the same protocol runs on gloo +
   CPU tensors in the tests, with the oracle as the step engine.
 
+* overlap (north star tier 3): each round first launches the slab's interior
+  planes, whose k-step dependency cone stays inside the owned planes, while
+  the exchange runs on a separate CUDA stream; the 2*depth seam planes are
+  launched once the ghosts have landed (tsr_sweep_range, the reference's
+  "compute interior of step 0 -> recv and install ghost -> finish seam"
+  ordering of HaloWorker::run_round, scheduler.cpp:371-406).
+
 Seam-side halo planes of a local slab are beyond the ghost region and never
 influence owned rows; ``poison=True`` fills them with NaN to prove it (the
 reference's run_heterogeneous_instrumented, scheduler.cpp:410-421).
@@ -128,14 +135,49 @@ class _DeviceState:
         self.fused_steps = fused_steps
         self.mode = mode
         self.h0 = host_local.halo[0]
-        self.plane = self.dg.layout.pitch[0] if len(host_local.extent) > 1 else 1
+        # element offset of local plane `row`: whole padded planes for 2-D/3-D;
+        # a 1-D row is one element, its interior starts at the layout origin
+        if len(host_local.extent) > 1:
+            self.plane, self.base = self.dg.layout.pitch[0], self.h0 * self.dg.layout.pitch[0]
+        else:
+            self.plane, self.base = 1, self.dg.layout.origin
 
     def advance(self, n):
         return self.dg.advance(self.kernel, n, fused_steps=self.fused_steps, mode=self.mode)
 
+    # -- overlapped rounds (tsr_sweep_range on two streams) ---------------
+    def comm_stream(self):
+        if not hasattr(self, "_xs"):
+            torch = self.dg.torch
+            self._xs = torch.cuda.Stream(device=self.dg.device)
+            self._ev_ready = torch.cuda.Event()
+            self._ev_comm = torch.cuda.Event()
+        return self._xs
+
+    def round_begin(self):
+        """The comm stream may touch the current buffer once every launch
+        that wrote it (the previous round) has finished."""
+        torch = self.dg.torch
+        xs = self.comm_stream()
+        self._ev_ready.record(torch.cuda.current_stream(self.dg.device))
+        xs.wait_event(self._ev_ready)
+        return torch.cuda.stream(xs)
+
+    def comm_done(self):
+        torch = self.dg.torch
+        self._ev_comm.record(self._xs)
+        torch.cuda.current_stream(self.dg.device).wait_event(self._ev_comm)
+
+    def sweep_range(self, lo, hi, n):
+        return self.dg.sweep_range(self.kernel, lo, hi, n, fused_steps=self.fused_steps,
+                                   mode=self.mode)
+
+    def flip(self, n):
+        self.dg.flip(n)
+
     def planes(self, row: int, count: int):
         """Contiguous view of local planes [row, row+count) of the current buffer."""
-        start = (row + self.h0) * self.plane
+        start = self.base + row * self.plane
         return self.dg.buf[self.dg.cur][start:start + count * self.plane]
 
     def sync(self):
@@ -171,13 +213,34 @@ class _HostState:
     def sync(self):
         pass
 
+    # overlapped rounds on the host: the same range / flip protocol, one
+    # pass of n steps per range computed on a scratch copy
+    def round_begin(self):
+        import contextlib
+        return contextlib.nullcontext()
+
+    def comm_done(self):
+        pass
+
+    def sweep_range(self, lo, hi, n):
+        if hi <= lo:
+            return 0
+        tmp = self.g.copy()
+        self.step_fn(tmp, n)
+        h = self.h0
+        self.g.padded(1 - self.g.parity)[lo + h:hi + h] = tmp.padded(tmp.parity)[lo + h:hi + h]
+        return 0
+
+    def flip(self, n):
+        self.g.flip_parity()
+
 
 class SlabRunner:
     """Round driver for one rank (HaloWorker::run_round generalised to P
     slabs).  ``advance(n)`` runs one round of n <= k steps: exchange the
     ghost planes with both neighbours, then n fused steps on the local slab."""
 
-    def __init__(self, plan: SlabPlan, state, group=None):
+    def __init__(self, plan: SlabPlan, state, group=None, overlap: bool = True):
         import torch.distributed as dist
         self.dist = dist
         # gloo cannot move CUDA tensors point-to-point: stage through host
@@ -189,6 +252,7 @@ class SlabRunner:
         self.state = state
         self.group = group
         self.fused_steps = plan.fused_steps
+        self.overlap = overlap
         self.round = 0
         self.log = CommLog()
         self.exchange_bytes = 0
@@ -196,13 +260,13 @@ class SlabRunner:
     # -- constructors -----------------------------------------------------
     @classmethod
     def on_device(cls, ts, kernel, plan: SlabPlan, host_local, device, mode="exact",
-                  group=None):
+                  group=None, overlap=True):
         return cls(plan, _DeviceState(ts, kernel, host_local, device, plan.fused_steps, mode),
-                   group)
+                   group, overlap)
 
     @classmethod
     def synthetic(cls, ts, kernel, plan: SlabPlan, dtype, device, seed=1, fused_steps=None,
-                  mode="exact", group=None):
+                  mode="exact", group=None, overlap=True):
         """Benchmark slab: the local grid is filled with fill_random(seed)
         directly (no global host grid); the first exchange makes the ghost
         planes consistent with the neighbours."""
@@ -217,11 +281,11 @@ class SlabRunner:
                               plan.halo, esize)
         host = cls_(plan.local_extent, plan.halo)
         ts.fill_random(host, seed)
-        return cls.on_device(ts, kernel, plan, host, device, mode, group)
+        return cls.on_device(ts, kernel, plan, host, device, mode, group, overlap)
 
     @classmethod
-    def on_host(cls, plan: SlabPlan, host_local, step_fn, group=None):
-        return cls(plan, _HostState(host_local, step_fn), group)
+    def on_host(cls, plan: SlabPlan, host_local, step_fn, group=None, overlap=False):
+        return cls(plan, _HostState(host_local, step_fn), group, overlap)
 
     # -- protocol ---------------------------------------------------------
     def exchange(self):
@@ -257,12 +321,45 @@ class SlabRunner:
         for _, t in sends:
             self.exchange_bytes += t.numel() * t.element_size()
 
+    def ranges(self, n: int):
+        """(interior, seams) plane ranges of one overlapped round in local
+        interior coordinates: the interior's n-step cone stays inside the
+        owned planes; the seams need the ghosts."""
+        p = self.plan
+        dl = p.radius * n if p.ghost_lo else 0
+        dh = p.radius * n if p.ghost_hi else 0
+        lo, hi = p.ghost_lo, p.ghost_lo + p.own
+        if hi - lo <= dl + dh:
+            return (lo, lo), [(lo, hi)]
+        return (lo + dl, hi - dh), [(lo, lo + dl), (hi - dh, hi)]
+
+    def _round_overlapped(self, n: int):
+        """HaloWorker::run_round's order (scheduler.cpp:371-406) on two
+        streams: exchange on the comm stream || interior planes on the
+        compute stream, then the seam planes once the ghosts are in."""
+        st = self.state
+        with st.round_begin():
+            self.exchange()
+        (ilo, ihi), seams = self.ranges(n)
+        launches = st.sweep_range(ilo, ihi, n)
+        st.comm_done()
+        for lo, hi in seams:
+            launches += st.sweep_range(lo, hi, n)
+        st.flip(n)
+
+        class _S:
+            kernel_launches = launches
+        return _S()
+
     def advance(self, n: int):
         if n > self.fused_steps:
             raise ValueError("a round advances at most k = depth / r steps")
-        if self.plan.world > 1:
-            self.exchange()
-        st = self.state.advance(n)
+        if self.plan.world > 1 and self.overlap:
+            st = self._round_overlapped(n)
+        else:
+            if self.plan.world > 1:
+                self.exchange()
+            st = self.state.advance(n)
         # ghost planes recomputed by this rank (HaloWorker::tally_ghost)
         cross = 1
         for e in self.plan.global_extent[1:]:
@@ -291,7 +388,8 @@ class SlabRunner:
         return g.padded(g.parity)[h0 + self.plan.ghost_lo:h0 + self.plan.ghost_lo + self.plan.own]
 
     def comm_summary(self) -> dict:
-        return {"rounds": self.round, "messages_sent": len(self.log.records),
+        return {"rounds": self.round, "overlap": bool(self.overlap and self.plan.world > 1),
+                "messages_sent": len(self.log.records),
                 "bytes_per_message": self.plan.bytes_per_message,
                 "halo_depth": self.plan.depth, "fused_steps": self.fused_steps,
                 "bytes_sent": self.exchange_bytes,

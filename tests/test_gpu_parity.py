@@ -254,3 +254,39 @@ def test_full_shape_properties(ts, orc, cfg):
     ts.run_gpu(c, k, 2, fused_steps=fused, mode="exact")
     orc.naive_run(d, k, 2)
     assert both_buffers_equal(c, d)
+
+
+@pytest.mark.parametrize("name,extent,fused,dt", [
+    ("Heat-3D", [90, 40, 70], 3, "f64"),     # tb3d, several a0 chunks
+    ("Heat-3D", [50, 33, 41], 2, "f32"),
+    ("Box-3D27P", [60, 30, 50], 1, "f32"),   # box3d
+    ("Box-3D27P", [60, 30, 50], 2, "f64"),   # box3d two-level
+    ("Box-2D9P", [200, 150], 4, "f64"),     # stream2d: the range is along the rows
+    ("Heat-2D", [120, 90], 6, "f32"),
+    ("Heat-1D", [500], 1, "f64"),           # generic
+])
+def test_sweep_range_stores_only_its_planes(ts, orc, name, extent, fused, dt):
+    """tsr_sweep_range: planes [lo, hi) of axis 0 hold the k-step result
+    bitwise, every other cell of the output buffer is left untouched (NaN
+    sentinel), for ranges at the low edge, in the middle, at the high edge."""
+    import torch
+    k = ts.find_benchmark(name).kernel
+    g = random_grid(ts, orc, extent, [k.radius] * k.dims, 11, dt)
+    ref = g.copy()
+    orc.naive_run(ref, k, fused)
+    want = ref.interior_view(ref.parity)
+    n0 = extent[0]
+    for lo, hi in [(0, 7), (n0 // 3, n0 // 3 + 13), (n0 - 5, n0), (0, n0), (4, 4)]:
+        dg = ts.DeviceGrid(g, torch.device("cuda", 0))
+        dg.buf[1 - dg.cur].fill_(float("nan"))
+        dg.sweep_range(k, lo, hi, fused, fused_steps=fused)
+        dg.flip(fused)
+        got = g.copy()
+        dg.download(got)
+        cur = got.interior_view(got.parity)
+        assert cur[lo:hi].tobytes() == want[lo:hi].tobytes(), (lo, hi)
+        assert np.isnan(cur[:lo]).all() and np.isnan(cur[hi:]).all(), (lo, hi)
+    with pytest.raises(ValueError):
+        dg.sweep_range(k, 0, n0 + 1, fused, fused_steps=fused)
+    with pytest.raises(ValueError):
+        dg.sweep_range(k, 0, n0, fused + 1, fused_steps=fused)

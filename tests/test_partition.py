@@ -21,7 +21,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, name, extent, steps, k, poison, out_dir):
+def _worker(rank, world, port, name, extent, steps, k, poison, out_dir, overlap=False):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     import oracle
@@ -36,7 +36,8 @@ def _worker(rank, world, port, name, extent, steps, k, poison, out_dir):
     orc.fill_random(glob, 500)
     plan = plan_slabs(extent, kern.radius, k, world, rank)
     loc = local_from_global(glob, plan, poison=poison)
-    runner = SlabRunner.on_host(plan, loc, lambda g, n: orc.naive_run(g, kern, n))
+    runner = SlabRunner.on_host(plan, loc, lambda g, n: orc.naive_run(g, kern, n),
+                                overlap=overlap)
     runner.run(steps)
     np.save(os.path.join(out_dir, f"own{rank}.npy"), runner.own_rows())
     np.save(os.path.join(out_dir, f"log{rank}.npy"),
@@ -45,24 +46,28 @@ def _worker(rank, world, port, name, extent, steps, k, poison, out_dir):
     dist.destroy_process_group()
 
 
-def _run(tmp_path, world, name, extent, steps, k, poison=True):
+def _run(tmp_path, world, name, extent, steps, k, poison=True, overlap=False):
     port = _free_port()
     mp.start_processes(_worker, args=(world, port, name, extent, steps, k, poison,
-                                      str(tmp_path)), nprocs=world, join=True,
+                                      str(tmp_path), overlap), nprocs=world, join=True,
                        start_method="spawn")
     return ([np.load(tmp_path / f"own{r}.npy") for r in range(world)],
             [np.load(tmp_path / f"log{r}.npy") for r in range(world)])
 
 
+@pytest.mark.parametrize("overlap", [False, True], ids=["serial", "overlap"])
 @pytest.mark.parametrize("world,name,extent,steps,k", [
     (2, "Heat-2D", [128, 64], 6, 3),      # test_scheduler.cpp:137-158's shape
     (2, "Box-2D9P", [80, 24], 5, 2),
     (3, "Heat-2D", [61, 37], 7, 3),
     (3, "Heat-3D", [30, 9, 11], 5, 2),
     (2, "Star-2D9P", [48, 20], 6, 4),
+    (3, "Heat-2D", [13, 20], 5, 2),      # slabs of 4-5 planes: no interior range
 ])
-def test_slabs_equal_oracle_bitwise(ts, orc, tmp_path, world, name, extent, steps, k):
-    own, logs = _run(tmp_path, world, name, extent, steps, k)
+def test_slabs_equal_oracle_bitwise(ts, orc, tmp_path, world, name, extent, steps, k, overlap):
+    """Serial rounds (exchange, then the whole slab) and overlapped rounds
+    (interior range, exchange, seam ranges) are both bitwise naive_run."""
+    own, logs = _run(tmp_path, world, name, extent, steps, k, overlap=overlap)
     kern = ts.find_benchmark(name).kernel
     ref = ts.Grid(extent, [kern.radius] * len(extent))
     orc.fill_random(ref, 500)
@@ -91,7 +96,7 @@ def test_reference_message_and_ghost_counts(ts, orc, tmp_path):
         plan_slabs([8, 8], 1, 5, 2, 0)  # subdomain smaller than the halo depth
 
 
-def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir):
+def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, overlap):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -108,7 +113,7 @@ def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir):
     orc.fill_random(glob, 500)
     plan = plan_slabs(extent, kern.radius, k, world, rank)
     loc = local_from_global(glob, plan, poison=True)
-    runner = SlabRunner.on_device(ts, kern, plan, loc, torch.device("cuda", 0))
+    runner = SlabRunner.on_device(ts, kern, plan, loc, torch.device("cuda", 0), overlap=overlap)
     runner.run(steps)
     np.save(os.path.join(out_dir, f"own{rank}.npy"), runner.own_rows(loc))
     np.save(os.path.join(out_dir, f"log{rank}.npy"),
@@ -118,16 +123,22 @@ def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("overlap", [False, True], ids=["serial", "overlap"])
 @pytest.mark.parametrize("world,name,extent,steps,k", [
     (2, "Heat-3D", [70, 40, 67], 7, 3),   # tb3d engine on each slab
     (3, "Box-2D9P", [90, 130], 9, 4),    # stream2d engine
     (2, "Box-3D27P", [40, 30, 50], 4, 1),  # box3d engine
+    (2, "Box-3D27P", [44, 30, 50], 5, 2),  # box3d two-level engine
+    (3, "Heat-1D", [300], 6, 1),          # generic engine, 1-D slabs
 ])
-def test_slabs_on_device_equal_oracle(ts, orc, tmp_path, world, name, extent, steps, k):
-    """The device slab state (pitched HBM buffers, tsr_advance, zero-copy
-    plane views) with several ranks sharing one GPU over gloo."""
+def test_slabs_on_device_equal_oracle(ts, orc, tmp_path, world, name, extent, steps, k,
+                                      overlap):
+    """The device slab state (pitched HBM buffers, tsr_advance or
+    tsr_sweep_range on two streams, zero-copy plane views) with several ranks
+    sharing one GPU over gloo."""
     port = _free_port()
-    mp.start_processes(_gpu_worker, args=(world, port, name, extent, steps, k, str(tmp_path)),
+    mp.start_processes(_gpu_worker, args=(world, port, name, extent, steps, k, str(tmp_path),
+                                          overlap),
                        nprocs=world, join=True, start_method="spawn")
     kern = ts.find_benchmark(name).kernel
     ref = ts.Grid(extent, [kern.radius] * len(extent))
