@@ -73,11 +73,67 @@ class CaseStudyConfig:
 
 
 def apply_full_scale(cfg: CaseStudyConfig) -> None:
-    """case_study.cpp:118-125: 9600 x 9600, 3.8e6 steps, checkpoint at the end."""
+    """case_study.cpp:118-123: 9600 x 9600, 3.8e6 steps, checkpoints at 1e6,
+    2e6 and 3.8e6."""
     cfg.extent = 9600
     cfg.steps = 3_800_000
-    cfg.checkpoints = [cfg.steps]
+    cfg.checkpoints = [1_000_000, 2_000_000, 3_800_000]
     cfg.sample_every = 10_000
+
+
+def parse_case_config(path: str) -> CaseStudyConfig:
+    """Line-oriented ``key = value`` config (case_study.cpp:74-116): '#'
+    comments, the reference's keys; an unknown key or a line without '='
+    raises RuntimeError naming the line.  ``path`` may only name an executor
+    this library runs (gpu/naive/tessellate, all on the B200); ``threads`` is
+    accepted and ignored (the CUDA grid replaces the worker threads)."""
+    cfg = CaseStudyConfig()
+    full = False
+    try:
+        f = open(path)
+    except OSError:
+        raise RuntimeError(f"cannot open config: {path}") from None
+    with f:
+        for lineno, line in enumerate(f, 1):
+            line = line.split("#", 1)[0].strip()
+            if not line:
+                continue
+            if "=" not in line:
+                raise RuntimeError(f"config line {lineno}: expected key = value")
+            key, value = (t.strip() for t in line.split("=", 1))
+            if key == "extent":
+                cfg.extent = int(value)
+            elif key == "steps":
+                cfg.steps = int(value)
+            elif key == "mu":
+                cfg.mu = float(value)
+            elif key == "peak":
+                cfg.peak_celsius = float(value)
+            elif key == "ambient":
+                cfg.ambient_celsius = float(value)
+            elif key == "sigma":
+                cfg.sigma_cells = float(value)
+            elif key == "plate_side_mm":
+                cfg.plate_side_mm = float(value)
+            elif key == "path":
+                if value not in ("gpu", "naive", "tessellate"):
+                    raise ValueError(f"unsupported executor path on the GPU library: {value}")
+            elif key == "threads":
+                int(value)
+            elif key == "sample_every":
+                cfg.sample_every = int(value)
+            elif key == "full":
+                full = value in ("1", "true")
+            elif key == "checkpoints":
+                cfg.checkpoints = [int(t.strip()) for t in value.split(",")]
+            elif key in ("fused_steps", "mode"):  # GPU extensions
+                setattr(cfg, key, int(value) if key == "fused_steps" else value)
+            else:
+                raise RuntimeError(f"config line {lineno}: unknown key '{key}'")
+    if full:
+        apply_full_scale(cfg)
+    heat_coefficients(cfg.mu)  # rejects an unstable CFL number here
+    return cfg
 
 
 def _init(grid, cfg: CaseStudyConfig, sigma: float) -> None:

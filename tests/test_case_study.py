@@ -26,7 +26,7 @@ def test_config_validation(ts):
                                                   case_study_heat)
     cfg = CaseStudyConfig()
     apply_full_scale(cfg)
-    assert (cfg.extent, cfg.steps, cfg.checkpoints) == (9600, 3_800_000, [3_800_000])
+    assert (cfg.extent, cfg.steps, cfg.checkpoints) == (9600, 3_800_000, [1_000_000, 2_000_000, 3_800_000])
     with pytest.raises(ValueError):
         case_study_heat(CaseStudyConfig(extent=8))
     with pytest.raises(ValueError):
