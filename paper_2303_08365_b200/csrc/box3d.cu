@@ -177,10 +177,7 @@ __global__ void __launch_bounds__(NT) box3d_kernel(T* __restrict__ out,
             T* o = out + a.origin + (long long)po * a.pitch0 + (long long)(gy + y) * a.pitch1 +
                    (gx + x);
 #pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
-#pragma unroll
-                for (int cx = 0; cx < VX; ++cx)
-                    if (ok[cy][cx]) o[cy * a.pitch1 + cx] = accB[cy][cx];
+            for (int cy = 0; cy < VY; ++cy) store_row<T, VX>(o + cy * a.pitch1, accB[cy], ok[cy]);
         }
         // output q continues (di = 0), output q+1 starts (di = -1)
         apply9<EXACT, false>(a.w + 9, nb, accA);
@@ -362,10 +359,12 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
             T* o = out + a.origin + (long long)po * a.pitch0 + (long long)(gy + y) * a.pitch1 +
                    (gx + x);
 #pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
+            for (int cy = 0; cy < VY; ++cy) {
+                T v[VX];
 #pragma unroll
-                for (int cx = 0; cx < VX; ++cx)
-                    if (cout[cy][cx]) o[cy * a.pitch1 + cx] = fix_zero<EXACT>(a2B[cy][cx]);
+                for (int cx = 0; cx < VX; ++cx) v[cx] = fix_zero<EXACT>(a2B[cy][cx]);
+                store_row<T, VX>(o + cy * a.pitch1, v, cout[cy]);
+            }
         }
         apply9<EXACT, false>(a.w + 9, nb2, a2A);
 #pragma unroll

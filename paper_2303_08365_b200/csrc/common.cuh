@@ -118,6 +118,38 @@ __device__ __forceinline__ T fix_zero(T v) {
     else return v;
 }
 
+// N consecutive outputs of one row: vector stores (16 B, or N elements when
+// shorter) wherever a whole vector is inside the output tile, scalar
+// predicated stores at its ragged edge.  `o` must be vector aligned: device rows start interior column 0 on a
+// 128-B boundary and every engine's column offsets are vector multiples.
+template <typename T, int N>
+__device__ __forceinline__ void store_row(T* o, const T (&v)[N], const bool (&ok)[N]) {
+    constexpr int NV = (16 / (int)sizeof(T)) < N ? 16 / (int)sizeof(T) : N;  // vector width
+    static_assert(N % NV == 0, "row length must be a multiple of the vector");
+#pragma unroll
+    for (int c = 0; c < N; c += NV) {
+        bool all = true;
+#pragma unroll
+        for (int u = 0; u < NV; ++u) all &= ok[c + u];
+        if (all) {
+            if constexpr (sizeof(T) == 8 && NV == 2) {
+                *reinterpret_cast<double2*>(o + c) = make_double2(v[c], v[c + 1]);
+            } else if constexpr (sizeof(T) == 4 && NV == 4) {
+                *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+            } else if constexpr (sizeof(T) == 4 && NV == 2) {
+                *reinterpret_cast<float2*>(o + c) = make_float2(v[c], v[c + 1]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < NV; ++u) o[c + u] = v[c + u];
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < NV; ++u)
+                if (ok[c + u]) o[c + u] = v[c + u];
+        }
+    }
+}
+
 // Compile-time loop: f(std::integral_constant<int, i>) for i in [0, N).
 template <int I, int N, typename F>
 __device__ __forceinline__ void static_for(F&& f) {

@@ -4,20 +4,24 @@
 //  * Memory tier: each CTA owns an output tile of (32-2(K-1)) x (64-2(K-1))
 //    cells of the (a1, a2) plane and streams a chunk of a0 planes.  Level-0
 //    planes (the tile plus a (K-1)+1 halo ring) arrive by TMA
-//    (cp.async.bulk.tensor.3d) into a 4-stage shared-memory ring guarded by
-//    mbarriers, three planes ahead of use.
-//  * SMEM tier (locality enhancer): levels 1..K-1 are computed on shrinking
-//    regions (overlapped tiling, the halo shrinks by one cell per level) as
-//    a wavefront along a0 — level l works on plane t-l while plane t
-//    arrives — so K steps cost one HBM read and one HBM write per cell.
-//    Each level's newest plane sits in a double-buffered SMEM plane for the
-//    a1-neighbours of other warps; one __syncthreads per plane serves all K
+//    (cp.async.bulk.tensor.3d) into a 5-stage shared-memory ring guarded by
+//    mbarriers (planes t-2 .. t+2 of step t).
+//  * SMEM tier (locality enhancer): levels 1..K-1 are computed on the same
+//    region (overlapped tiling: the valid part shrinks by one cell per level)
+//    as a wavefront along a0 — level l works on plane t-2l — so K steps cost
+//    one HBM read and one HBM write per cell.  The two-plane skew makes the
+//    K levels' dependency chains independent within a step; each level's
+//    newest plane goes to a 3-deep SMEM buffer for the a1-neighbours of other
+//    warps, read two steps later; one __syncthreads per plane serves all K
 //    levels.
 //  * Register tier (pattern mapping): a thread owns a 2 (a1) x 2 (a2) stack
-//    of columns and keeps, per level, the previous and current plane in
-//    registers (the a0-neighbours); a2-neighbours come from the adjacent lane
-//    by warp shuffle, a1-neighbours inside the stack from its own registers.
-//
+//    of columns and keeps, per level, a three-plane window in registers (the
+//    a0-neighbours), rotated by renaming (step loop unrolled by 3);
+//    a2-neighbours come from the adjacent lane by warp shuffle,
+//    a1-neighbours inside the stack from its own registers.
+//  * Boundary handling is decided per warp and per 3-step unit: warps with no
+//    boundary column whose planes are all interior run a select-free
+//    instantiation (no Dirichlet selects, no store-range check).
 // Per point and level the arithmetic is apply_box's
 // (proj/include/tessera/naive.hpp:69-82): acc = 0, then the seven taps in
 // canonical order (-1,0,0) (0,-1,0) (0,0,-1) (0,0,0) (0,0,1) (0,1,0) (1,0,0).
@@ -34,15 +38,25 @@ namespace tsr {
 namespace {
 
 constexpr int R1X = 64;  // level-1 region width  (a2)
-constexpr int R1Y = 32;  // level-1 region height (a1)
 constexpr int VX = 2;    // columns per thread along a2
-constexpr int VY = 2;    // columns per thread along a1
 constexpr int NLX = R1X / VX;  // 32 lanes
-constexpr int NLY = R1Y / VY;  // 16 warps
-constexpr int NT = NLX * NLY;  // 512 threads
-constexpr int BY0 = R1Y + 2;   // TMA box height: 1 extra row per side
 constexpr int STAGES = 5;  // planes t-2 .. t+2 of the level-0 ring
-constexpr int LEVY = R1Y + 2;  // level buffer rows (1 padding row per side)
+
+// Region height and column-stack depth: a warp owns VY rows of the R1Y-row
+// level-1 region, so a CTA has R1Y / VY warps.
+template <int VY_, int R1Y_>
+struct Shape {
+    static constexpr int VY = VY_;          // columns per thread along a1
+    static constexpr int R1Y = R1Y_;        // level-1 region height (a1)
+    static constexpr int NLY = R1Y / VY;    // warps
+    static constexpr int NT = NLX * NLY;    // threads
+    static constexpr int BY0 = R1Y + 2;     // TMA box height: 1 extra row per side
+    static constexpr int LEVY = R1Y + 2;    // level buffer rows (1 padding row per side)
+};
+// 512 threads, 2x2 columns per thread.  A 4x2 stack with 256 threads
+// (half the SMEM traffic per point, 186-239 registers) measured 2-4% slower
+// in exact mode: 8 warps per SM hide too little latency.
+using ShapeA = Shape<2, 32>;
 
 template <typename T>
 struct Pair;
@@ -69,18 +83,18 @@ constexpr int HXL = (K - 1 + VEC<T> - 1) / VEC<T> * VEC<T>;  // left overlap
 template <typename T, int K>
 constexpr int TXO = (R1X - HXL<T, K> - (K - 1)) / VEC<T> * VEC<T>;  // output tile width
 
-template <typename T>
+template <typename T, typename G>
 constexpr int slot_bytes() {
-    return (BX0<T> * BY0 * (int)sizeof(T) + 1023) / 1024 * 1024;
+    return (BX0<T> * G::BY0 * (int)sizeof(T) + 1023) / 1024 * 1024;
 }
-template <typename T>
+template <typename T, typename G>
 constexpr int lev_bytes() {
-    return (LEVY * R1X * (int)sizeof(T) + 127) / 128 * 128;
+    return (G::LEVY * R1X * (int)sizeof(T) + 127) / 128 * 128;
 }
 constexpr int NLEV = 3;  // level-l planes are read two steps after they are written
-template <typename T, int K>
+template <typename T, int K, typename G>
 constexpr int smem_bytes() {
-    return STAGES * slot_bytes<T>() + NLEV * (K - 1) * lev_bytes<T>() + STAGES * 8;
+    return STAGES * slot_bytes<T, G>() + NLEV * (K - 1) * lev_bytes<T, G>() + STAGES * 8;
 }
 
 template <typename T>
@@ -124,17 +138,28 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 // (q - t_begin) % 3 == s, so the window rotates by renaming (loop unrolled
 // by 3).  a1-neighbour rows of other warps are read two steps after they
 // were written (3-deep SMEM buffers, one __syncthreads per step).
-template <typename T, int K, bool EXACT, int PH, bool SEL>
+template <typename T, int K, bool EXACT, int PH, bool SEL, typename G, bool EARLY0>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
                                           uint64_t* bar, int it, int t_begin, int i0, int i1,
                                           int lx, int x, int y, int gx, int gy,
-                                          const bool (&cint)[VY][VX], const bool (&cout)[VY][VX],
-                                          T (&Hs)[K][3][VY][VX]) {
+                                          const bool (&cint)[G::VY][VX],
+                                          const bool (&cout)[G::VY][VX],
+                                          T (&Hs)[K][3][G::VY][VX]) {
+    constexpr int VY = G::VY;
     using P2 = typename Pair<T>::type;
-    constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
-    constexpr int LEV = lev_bytes<T>() / (int)sizeof(T);
+    constexpr int SLOT = slot_bytes<T, G>() / (int)sizeof(T);
+    constexpr int LEV = lev_bytes<T, G>() / (int)sizeof(T);
     constexpr int BX = BX0<T>, PL = PADL<T>;
     const int t = t_begin + it;
+    const int slot = it % STAGES;
+    const T* P0 = ring + slot * SLOT;
+    P2 early[VY];
+    if constexpr (EARLY0) {  // level-0 rows of plane t fetched before the levels' math
+        mbar_wait(&bar[slot], (it / STAGES) & 1);
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+            early[cy] = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
+    }
 
 #pragma unroll
     for (int l = K; l >= 1; --l) {
@@ -187,45 +212,50 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
             T* L = lev + ((l - 1) * NLEV + sC) * LEV;
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy) {
-                P2 v;
-                v.x = res[cy][0];
-                v.y = res[cy][1];
-                *reinterpret_cast<P2*>(L + (y + cy + 1) * R1X + x) = v;
+                // only a warp's first and last rows are read by other warps
+                if (cy == 0 || cy == VY - 1) {
+                    P2 v;
+                    v.x = res[cy][0];
+                    v.y = res[cy][1];
+                    *reinterpret_cast<P2*>(L + (y + cy + 1) * R1X + x) = v;
+                }
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) Hs[l][sC][cy][cx] = res[cy][cx];
             }
-        } else if (p >= i0 && p < i1) {
+        } else if (!SEL || (p >= i0 && p < i1)) {  // !SEL: the caller checked the range
             T* o = out + a.origin + (long long)p * a.pitch0 + (long long)(gy + y) * a.pitch1 +
                    (gx + x);
 #pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
+            for (int cy = 0; cy < VY; ++cy) {
+                T v[VX];
 #pragma unroll
-                for (int cx = 0; cx < VX; ++cx)
-                    if (cout[cy][cx]) o[cy * a.pitch1 + cx] = fix_zero<EXACT>(res[cy][cx]);
+                for (int cx = 0; cx < VX; ++cx) v[cx] = fix_zero<EXACT>(res[cy][cx]);
+                store_row<T, VX>(o + cy * a.pitch1, v, cout[cy]);
+            }
         }
     }
     // Level 0 last: plane t into the window slot level 1 has just consumed.
-    const int slot = it % STAGES;
-    mbar_wait(&bar[slot], (it / STAGES) & 1);
-    const T* P0 = ring + slot * SLOT;
+    if constexpr (!EARLY0) mbar_wait(&bar[slot], (it / STAGES) & 1);
 #pragma unroll
     for (int cy = 0; cy < VY; ++cy) {
-        const P2 v = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
+        const P2 v = EARLY0 ? early[cy]
+                            : *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
         Hs[0][PH][cy][0] = v.x;
         Hs[0][PH][cy][1] = v.y;
     }
 }
 
-template <typename T, int K, bool EXACT>
-__global__ void __launch_bounds__(NT, 1)
+template <typename T, int K, bool EXACT, typename G, bool EARLY0>
+__global__ void __launch_bounds__(G::NT, 1)
     tb3d_kernel(T* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
                 const __grid_constant__ TbArgs<T> a) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
+    constexpr int VY = G::VY, R1Y = G::R1Y, BY0 = G::BY0;
+    constexpr int SLOT = slot_bytes<T, G>() / (int)sizeof(T);
     T* ring = reinterpret_cast<T*>(smem);
-    T* lev = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T>());
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>() +
-                                                NLEV * (K - 1) * lev_bytes<T>());
+    T* lev = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T, G>());
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T, G>() +
+                                                NLEV * (K - 1) * lev_bytes<T, G>());
 
     const int tid = threadIdx.x;
     const int lx = tid & 31, ly = tid >> 5;
@@ -306,27 +336,33 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int cx = 0; cx < VX; ++cx) mine &= cint[cy][cx];
     const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in this warp
-    // Planes t-2K..t-2 all interior and no column of this warp on the a1/a2
-    // boundary: no Dirichlet selects needed in this step (warp-uniform).
+    // A unit of three steps runs select-free when the planes its levels read
+    // (t-2K .. t-2) are interior, no column of this warp is on the a1/a2
+    // boundary and every plane level K produces is one of this chunk's
+    // outputs (p = i0 + it - 3K in [i0, i1)); the conditions are monotone in
+    // `it`, so checking the unit's first and last step suffices.
+    // Warp-uniform, decided once per unit.
     auto clear = [&](int it) {
         const int t = t_begin + it;
-        return warp_int && t - 2 * K >= 0 && t - 2 < a.n0;
+        return t - 2 * K >= 0 && t - 2 < a.n0 && it >= 3 * K && it < 3 * K + (i1 - i0);
     };
-#define TB3D_STEP(PH, IT)                                                                    \
-    if (clear(IT))                                                                           \
-        tb3d_step<T, K, EXACT, PH, false>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x, \
-                                          y, gx, gy, cint, cout, Hs);                        \
-    else                                                                                     \
-        tb3d_step<T, K, EXACT, PH, true>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x,  \
-                                         y, gx, gy, cint, cout, Hs);                         \
+#define TB3D_STEP(PH, IT, SEL)                                                                \
+    tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x, y, gx, \
+                                       gy, cint, cout, Hs);                                    \
     after(IT);
     for (int it = 0; it < niter; it += 3) {
-        TB3D_STEP(0, it)
-        if (it + 1 < niter) {
-            TB3D_STEP(1, it + 1)
-        }
-        if (it + 2 < niter) {
-            TB3D_STEP(2, it + 2)
+        if (warp_int && clear(it) && clear(it + 2)) {
+            TB3D_STEP(0, it, false)
+            TB3D_STEP(1, it + 1, false)
+            TB3D_STEP(2, it + 2, false)
+        } else {
+            TB3D_STEP(0, it, true)
+            if (it + 1 < niter) {
+                TB3D_STEP(1, it + 1, true)
+            }
+            if (it + 2 < niter) {
+                TB3D_STEP(2, it + 2, true)
+            }
         }
     }
 #undef TB3D_STEP
@@ -343,23 +379,23 @@ bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused)
     return true;
 }
 
-template <typename T, int K, bool EXACT>
+template <typename T, int K, bool EXACT, typename G, bool EARLY0 = false>
 Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     const Geo& g = *c.g;
     CUtensorMap map;
-    Status s = make_tmap_3d<T>(g, in, BX0<T>, BY0, &map);
+    Status s = make_tmap_3d<T>(g, in, BX0<T>, G::BY0, &map);
     if (!s.ok()) return s;
     TbArgs<T> a;
     a.n0 = (int)g.n[0];
     a.n1 = (int)g.n[1];
     a.n2 = (int)g.n[2];
-    constexpr int TX = TXO<T, K>, TY = R1Y - 2 * (K - 1);
+    constexpr int TX = TXO<T, K>, TY = G::R1Y - 2 * (K - 1);
     a.tiles_x = (int)((g.n[2] + TX - 1) / TX);
     a.tiles_y = (int)((g.n[1] + TY - 1) / TY);
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
-    constexpr int bytes = smem_bytes<T, K>();
+    constexpr int bytes = smem_bytes<T, K, G>();
     int per_sm = 1, nsm = 148;
-    s = occupancy(tb3d_kernel<T, K, EXACT>, NT, bytes, &per_sm, &nsm);
+    s = occupancy(tb3d_kernel<T, K, EXACT, G, EARLY0>, G::NT, bytes, &per_sm, &nsm);
     if (!s.ok()) return s;
     // a0 chunks: whole waves of resident CTAs, >= 48 planes (the 2K-plane
     // wavefront fill is overhead)
@@ -377,7 +413,7 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     for (int q = 0; q < 7; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     const long long nchunks = (span + a.chunk - 1) / a.chunk;
     const unsigned grid = (unsigned)(tiles * nchunks);
-    tb3d_kernel<T, K, EXACT><<<grid, NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);
+    tb3d_kernel<T, K, EXACT, G, EARLY0><<<grid, G::NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
 }
@@ -385,9 +421,10 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
 template <typename T, bool EXACT>
 Status launch_m(const LaunchCtx& c, const void* in, void* out, int k) {
     switch (k) {
-        case 1: return launch_k<T, 1, EXACT>(c, in, out);
-        case 2: return launch_k<T, 2, EXACT>(c, in, out);
-        case 3: return launch_k<T, 3, EXACT>(c, in, out);
+        case 1: return launch_k<T, 1, EXACT, ShapeA>(c, in, out);
+        case 2: return launch_k<T, 2, EXACT, ShapeA>(c, in, out);
+        case 3:
+            return launch_k<T, 3, EXACT, ShapeA, true>(c, in, out);
         default: return Status::Err(TSR_EUNSUPPORTED, "tb3d: fused steps must be 1..3");
     }
 }
