@@ -42,9 +42,23 @@ template <typename T>
 constexpr int slot_bytes() {
     return (BXW<T> * BY * (int)sizeof(T) + 127) / 128 * 128;
 }
+// The K = 1 kernel uses a wider tile: the TMA box of a 64-column fp32 tile
+// touches 10 DRAM sectors per row for 8 useful ones (the 1-cell halo plus the
+// 16-B aligned start add a sector each side), 128 columns make it 18 for 16.
+// fp64 keeps 64 columns (512 B rows, 4 CTAs per SM).
+template <typename T>
+constexpr int OX1 = sizeof(T) == 4 ? 128 : 64;
+template <typename T>
+constexpr int NT1 = OX1<T> / VX * NLY;  // 256 / 128 threads
+template <typename T>
+constexpr int BXW1 = OX1<T> + 2 * PAD<T>;
+template <typename T>
+constexpr int slot1_bytes() {
+    return (BXW1<T> * BY * (int)sizeof(T) + 127) / 128 * 128;
+}
 template <typename T>
 constexpr int smem_bytes() {
-    return STAGES * slot_bytes<T>() + STAGES * 8;
+    return STAGES * slot1_bytes<T>() + STAGES * 8;
 }
 
 template <typename T>
@@ -93,22 +107,23 @@ __device__ __forceinline__ void apply9(const T* __restrict__ w, const T (&nb)[VY
 }
 
 template <typename T, bool EXACT>
-__global__ void __launch_bounds__(NT) box3d_kernel(T* __restrict__ out,
-                                                  const __grid_constant__ CUtensorMap tmap,
-                                                  const __grid_constant__ BoxArgs<T> a) {
+__global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
+                                                   const __grid_constant__ CUtensorMap tmap,
+                                                   const __grid_constant__ BoxArgs<T> a) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
-    constexpr int BX = BXW<T>, PL = PAD<T>;
+    constexpr int SLOT = slot1_bytes<T>() / (int)sizeof(T);
+    constexpr int BX = BXW1<T>, PL = PAD<T>;
+    constexpr int NLX1 = OX1<T> / VX;
     T* ring = reinterpret_cast<T*>(smem);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>());
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot1_bytes<T>());
 
     const int tid = threadIdx.x;
-    const int lx = tid % NLX, ly = tid / NLX;
+    const int lx = tid % NLX1, ly = tid / NLX1;
     const int tile = blockIdx.x;
     const int bx = tile % a.tiles_x;
     const int by = (tile / a.tiles_x) % a.tiles_y;
     const int bz = tile / (a.tiles_x * a.tiles_y);
-    const int gx = bx * OX, gy = by * OY;  // interior coords of the tile origin
+    const int gx = bx * OX1<T>, gy = by * OY;  // interior coords of the tile origin
     const int i0 = a.lo0 + bz * a.chunk;
     const int i1 = min(i0 + a.chunk, a.hi0);
     // planes i0-1 .. i1 feed outputs i0 .. i1-1
@@ -387,13 +402,13 @@ template <typename T, bool EXACT>
 Status launch(const LaunchCtx& c, const void* in, void* out) {
     const Geo& g = *c.g;
     CUtensorMap map;
-    Status s = make_tmap_3d<T>(g, in, BXW<T>, BY, &map);
+    Status s = make_tmap_3d<T>(g, in, BXW1<T>, BY, &map);
     if (!s.ok()) return s;
     BoxArgs<T> a;
     a.n0 = (int)g.n[0];
     a.n1 = (int)g.n[1];
     a.n2 = (int)g.n[2];
-    a.tiles_x = (int)((g.n[2] + OX - 1) / OX);
+    a.tiles_x = (int)((g.n[2] + OX1<T> - 1) / OX1<T>);
     a.tiles_y = (int)((g.n[1] + OY - 1) / OY);
     a.h0 = (int)g.h[0];
     a.h1 = (int)g.h[1];
@@ -404,7 +419,7 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     for (int q = 0; q < 27; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     constexpr int bytes = smem_bytes<T>();
     int per_sm = 1, nsm = 148;
-    s = occupancy(box3d_kernel<T, EXACT>, NT, bytes, &per_sm, &nsm);
+    s = occupancy(box3d_kernel<T, EXACT>, NT1<T>, bytes, &per_sm, &nsm);
     if (!s.ok()) return s;
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
     a.lo0 = (int)c.range_lo();
@@ -413,7 +428,7 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     const int64_t span = a.hi0 - a.lo0;
     a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 2, 32);
     const long long nchunks = (span + a.chunk - 1) / a.chunk;
-    box3d_kernel<T, EXACT><<<(unsigned)(tiles * nchunks), NT, bytes, c.stream>>>(
+    box3d_kernel<T, EXACT><<<(unsigned)(tiles * nchunks), NT1<T>, bytes, c.stream>>>(
         static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
