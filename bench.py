@@ -132,13 +132,13 @@ def fused_groups(steps: int, k: int) -> list[int]:
 def ncu_traffic(cfg_name: str, kfused: int):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel, from the committed ncu launch list of this bench command
-    (profiles/ncu_traffic.json, written by tools/launch_summary.py), or None
-    when the committed capture is for another fused depth."""
+    (profiles/ncu_traffic.json, written by tools/launch_summary.py --traffic),
+    or None when the committed capture is for another fused depth."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f).get(cfg_name)
-        if d and (f", {kfused}, " in d["kernel"]):
+        if d and d.get("fused_steps") == kfused:
             return d
     except Exception:
         pass
@@ -376,7 +376,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic["bytes_per_launch"] if traffic else None,
-                     "traffic_source": (f"ncu launch list profiles/r01/{traffic['source']} "
+                     "traffic_source": (f"ncu launch list profiles/{traffic['source']} "
                                         f"({traffic['kernel']})") if traffic else None,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                      if peak_kind == "measured" else "fallback (B200_PROFILING.md)",

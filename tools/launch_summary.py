@@ -1,6 +1,7 @@
 """Summarise an ncu --metrics launch list (csv): per kernel, launches, mean
 time, mean DRAM read+write per launch, share of total time.  With --traffic
-CFG it also updates profiles/ncu_traffic.json[CFG] with the dominant kernel."""
+CFG K it also updates profiles/ncu_traffic.json[CFG] with the dominant kernel
+(K = its fused steps per launch, which bench.py matches before reporting it)."""
 import csv
 import json
 import os
@@ -47,13 +48,15 @@ if __name__ == "__main__":
     for r in res:
         print(f"{r['kernel'][:70]:70} n={r['launches']:4d} mean={r['mean_ns']/1e3:9.1f} us "
               f"share={r['share']*100:5.1f}% dram/launch={r['dram_bytes_per_launch']/1e9:.4f} GB")
-    if len(sys.argv) > 3 and sys.argv[2] == "--traffic":
-        cfg = sys.argv[3]
+    if len(sys.argv) > 4 and sys.argv[2] == "--traffic":
+        cfg, fused = sys.argv[3], int(sys.argv[4])
         tp = os.path.join(os.path.dirname(__file__), "..", "profiles", "ncu_traffic.json")
         data = json.load(open(tp)) if os.path.exists(tp) else {}
         top = res[0]
         data[cfg] = {"kernel": top["kernel"], "bytes_per_launch": round(top["dram_bytes_per_launch"]),
                      "read": round(top["dram_read_per_launch"]),
                      "write": round(top["dram_write_per_launch"]),
-                     "source": os.path.basename(path)}
+                     "fused_steps": fused,
+                     "source": os.path.relpath(os.path.abspath(path),
+                                               os.path.abspath(os.path.dirname(tp)))}
         json.dump(data, open(tp, "w"), indent=1)
