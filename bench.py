@@ -7,8 +7,10 @@ Default workload (N=1): BASELINE config C3, the north star's headline target —
 Heat-3D 7-point star fp64, 512^3 interior, halo 1, fill_random(seed=1), 1000
 time steps.  A "step" is one time step over the whole grid.  For N>1 every
 rank owns a 512^3 slab of a (512*N) x 512 x 512 grid (weak scaling, C5's
-slab + deep-halo scheme at C3's per-GPU size) and exchanges r*k-deep halos
-with its neighbours over NCCL once per k fused steps.
+slab + deep-halo scheme at C3's per-GPU size); once per k fused steps its seam
+pass stores the r*k boundary planes straight into the neighbours' ghost planes
+over CUDA-IPC peer memory (--transport peer, default) or they are sent with
+NCCL send/recv (--transport nccl).
 
 `value` is device-resident throughput (GStencil/s = points * K / time, the
 reference's Eq. 6, proj/src/metrics.cpp:8-20), timed with CUDA events on the
@@ -216,6 +218,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: exchange, then the whole slab (no interior/seam split)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1 halo exchange: seam passes storing into the neighbours' ghost "
+                         "planes over CUDA-IPC peer memory (default), or NCCL send/recv")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 path with ranks sharing one GPU")
     args = ap.parse_args()
@@ -275,9 +280,17 @@ def main():
         kfused_guess = fused_req if fused_req else 1
         glob = list(cfg["extent"]) if strong else [per_gpu[0] * world] + per_gpu[1:]
         plan = plan_slabs(glob, k.radius, kfused_guess, world, rank)
-        runner = SlabRunner.synthetic(ts, k, plan, cfg["dtype"], dev, seed=1 + rank,
-                                      fused_steps=fused_req, mode=mode,
-                                      overlap=not args.no_overlap)
+        try:
+            runner = SlabRunner.synthetic(ts, k, plan, cfg["dtype"], dev, seed=1 + rank,
+                                          fused_steps=fused_req, mode=mode,
+                                          overlap=not args.no_overlap, transport=args.transport)
+        except Exception as e:  # IPC mapping refused on this box: message transport
+            if args.transport != "peer":
+                raise
+            print(f"peer transport unavailable ({e}); using nccl", file=sys.stderr)
+            runner = SlabRunner.synthetic(ts, k, plan, cfg["dtype"], dev, seed=1 + rank,
+                                          fused_steps=fused_req, mode=mode,
+                                          overlap=not args.no_overlap, transport="nccl")
         kfused = runner.fused_steps
         engine = 2
         advance = runner.advance
@@ -348,6 +361,8 @@ def main():
         if not args.no_cpu:
             cpu = cpu_baseline(ts, cfg, args.config)
 
+    if comm is not None:
+        comm.close()
     if rank != 0:
         if dist:
             dist.destroy_process_group()

@@ -153,6 +153,35 @@ int tsr_advance(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, voi
 int tsr_sweep_range(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, const void* in,
                     void* out, int64_t lo, int64_t hi, int32_t steps, const tsr_opts* opts,
                     void* stream);
+/* tsr_sweep_range whose stores are also written to `mirror` (a buffer in the
+ * same layout, normally a neighbour slab's buffer mapped by tsr_ipc_open) at
+ * axis-0 plane p + mirror_planes: the seam pass of a slab round delivers its
+ * planes straight into the neighbour's ghost planes over NVLink, replacing
+ * SlabChannel's per-round message (proj/src/scheduler.cpp:142-194, 371-406).
+ * mirror == NULL is tsr_sweep_range. */
+int tsr_sweep_range_mirror(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l,
+                           const void* in, void* out, int64_t lo, int64_t hi, int32_t steps,
+                           const tsr_opts* opts, void* mirror, int64_t mirror_planes,
+                           void* stream);
+
+/* ---- peer-memory transport (one process per GPU) ---------------------- */
+/* CUDA IPC handle of the allocation that contains `ptr` (any device pointer,
+ * e.g. a torch tensor's data) and ptr's byte offset inside it. */
+typedef struct tsr_ipc_handle {
+    unsigned char bytes[64];
+} tsr_ipc_handle;
+int tsr_ipc_export(const void* ptr, tsr_ipc_handle* handle, int64_t* offset);
+/* Maps another process's allocation (peer access enabled lazily); *base is
+ * the allocation's base in this process.  tsr_ipc_close unmaps it. */
+int tsr_ipc_open(const tsr_ipc_handle* handle, void** base);
+int tsr_ipc_close(void* base);
+/* Stream-ordered round flags: tsr_peer_signal stores `value` to a 32-bit
+ * word (local or peer-mapped) with system-scope release once all earlier
+ * work on `stream` is complete; tsr_peer_wait holds back later work on
+ * `stream` until the word reaches `value` (wrap-around compare). */
+int tsr_peer_signal(void* flag, uint32_t value, void* stream);
+int tsr_peer_wait(const void* flag, uint32_t value, void* stream);
+
 /* Reports the engine (tsr_engine) and fused step count k tsr_advance /
  * tsr_run would use for this kernel, grid and opts (no device work). */
 int tsr_query_plan(const tsr_kernel* k, const tsr_grid* g, const tsr_opts* opts,

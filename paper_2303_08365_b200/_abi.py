@@ -26,6 +26,8 @@ EXPORTED = (
     "tsr_abi_version", "tsr_last_error", "tsr_release_cache", "tsr_check_kernel",
     "tsr_fill_random", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
     "tsr_copy_halo", "tsr_advance", "tsr_query_plan", "tsr_apply_box", "tsr_sweep_range",
+    "tsr_sweep_range_mirror", "tsr_ipc_export", "tsr_ipc_open", "tsr_ipc_close",
+    "tsr_peer_signal", "tsr_peer_wait",
 )
 
 
@@ -64,6 +66,10 @@ class TsrOpts(ctypes.Structure):
         ("engine", ctypes.c_int32),
         ("device", ctypes.c_int32),
     ]
+
+
+class TsrIpcHandle(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_ubyte * 64)]
 
 
 class TsrStats(ctypes.Structure):
@@ -125,6 +131,15 @@ def lib() -> ctypes.CDLL:
         L.tsr_sweep_range.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrLayout), c_void_p,
                                       c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                       p(TsrOpts), c_void_p]
+        L.tsr_sweep_range_mirror.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrLayout), c_void_p,
+                                             c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_int32, p(TsrOpts), c_void_p,
+                                             ctypes.c_int64, c_void_p]
+        L.tsr_ipc_export.argtypes = [c_void_p, p(TsrIpcHandle), p(ctypes.c_int64)]
+        L.tsr_ipc_open.argtypes = [p(TsrIpcHandle), p(c_void_p)]
+        L.tsr_ipc_close.argtypes = [c_void_p]
+        L.tsr_peer_signal.argtypes = [c_void_p, ctypes.c_uint32, c_void_p]
+        L.tsr_peer_wait.argtypes = [c_void_p, ctypes.c_uint32, c_void_p]
         for name in EXPORTED:
             if name not in ("tsr_abi_version", "tsr_last_error"):
                 getattr(L, name).restype = ctypes.c_int
@@ -169,6 +184,27 @@ def query_plan(kernel, grid_desc: TsrGrid, fused_steps: int = 0, mode: str = "ex
     check(L.tsr_query_plan(ctypes.byref(kernel.c_struct()), ctypes.byref(grid_desc),
                            ctypes.byref(opts), ctypes.byref(e), ctypes.byref(k)))
     return {1: "generic", 2: "tuned"}[e.value], k.value
+
+
+def ipc_export(ptr: int) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding `ptr`, byte offset
+    of `ptr` in it)."""
+    h, off = TsrIpcHandle(), ctypes.c_int64()
+    check(lib().tsr_ipc_export(ctypes.c_void_p(ptr), ctypes.byref(h), ctypes.byref(off)))
+    return bytes(h.bytes), off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    """Maps another process's allocation; returns its base address here."""
+    h = TsrIpcHandle()
+    ctypes.memmove(h.bytes, handle, 64)
+    base = ctypes.c_void_p()
+    check(lib().tsr_ipc_open(ctypes.byref(h), ctypes.byref(base)))
+    return base.value
+
+
+def ipc_close(base: int) -> None:
+    check(lib().tsr_ipc_close(ctypes.c_void_p(base)))
 
 
 def grid_desc(extent, halo, dtype: str = "f64") -> TsrGrid:

@@ -462,6 +462,14 @@ void fill_random_t(const Geo& g, T* b0, T* b1, uint64_t seed, double lo, double 
 
 using namespace tsr;
 
+namespace tsr {
+Status peer_signal(void* flag, unsigned value, cudaStream_t s);
+Status peer_wait(const void* flag, unsigned value, cudaStream_t s);
+Status ipc_export(const void* ptr, unsigned char* handle, int64_t* offset);
+Status ipc_open(const unsigned char* handle, void** base);
+Status ipc_close(void* base);
+}  // namespace tsr
+
 extern "C" {
 
 int tsr_abi_version(void) { return TSR_ABI_VERSION; }
@@ -569,6 +577,13 @@ int tsr_advance(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, voi
 int tsr_sweep_range(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l, const void* in,
                     void* out, int64_t lo, int64_t hi, int32_t steps, const tsr_opts* opts,
                     void* stream) {
+    return tsr_sweep_range_mirror(k, g, l, in, out, lo, hi, steps, opts, nullptr, 0, stream);
+}
+
+int tsr_sweep_range_mirror(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l,
+                           const void* in, void* out, int64_t lo, int64_t hi, int32_t steps,
+                           const tsr_opts* opts, void* mirror, int64_t mirror_planes,
+                           void* stream) {
     if (!k || !g || !in || !out) return report(Status::Err(TSR_EINVAL, "null argument"));
     if (in == out) return report(Status::Err(TSR_EINVAL, "in and out must be distinct buffers"));
     Geo geo;
@@ -590,7 +605,37 @@ int tsr_sweep_range(const tsr_kernel* k, const tsr_grid* g, const tsr_layout* l,
     LaunchCtx c{&geo, &t, o.mode != TSR_FAST, static_cast<cudaStream_t>(stream)};
     c.lo0 = lo;
     c.hi0 = hi;
+    if (mirror) {
+        if (mirror == out) return report(Status::Err(TSR_EINVAL, "mirror aliases out"));
+        c.mirror = mirror;
+        c.mirror_shift = mirror_planes * geo.pitch[3 - geo.dims];  // axis-0 planes -> elements
+    }
     return report(sweep(c, p, in, out, steps));
+}
+
+int tsr_peer_signal(void* flag, uint32_t value, void* stream) {
+    if (!flag) return report(Status::Err(TSR_EINVAL, "null flag"));
+    return report(peer_signal(flag, value, static_cast<cudaStream_t>(stream)));
+}
+
+int tsr_peer_wait(const void* flag, uint32_t value, void* stream) {
+    if (!flag) return report(Status::Err(TSR_EINVAL, "null flag"));
+    return report(peer_wait(flag, value, static_cast<cudaStream_t>(stream)));
+}
+
+int tsr_ipc_export(const void* ptr, tsr_ipc_handle* handle, int64_t* offset) {
+    if (!ptr || !handle || !offset) return report(Status::Err(TSR_EINVAL, "null argument"));
+    return report(ipc_export(ptr, handle->bytes, offset));
+}
+
+int tsr_ipc_open(const tsr_ipc_handle* handle, void** base) {
+    if (!handle || !base) return report(Status::Err(TSR_EINVAL, "null argument"));
+    return report(ipc_open(handle->bytes, base));
+}
+
+int tsr_ipc_close(void* base) {
+    if (!base) return report(Status::Err(TSR_EINVAL, "null argument"));
+    return report(ipc_close(base));
 }
 
 int tsr_query_plan(const tsr_kernel* k, const tsr_grid* g, const tsr_opts* opts,

@@ -68,6 +68,8 @@ struct BoxArgs {
     int lo0, hi0;  // output planes [lo0, hi0) of a0
     int h0, h1, off2;
     long long pitch0, pitch1, origin;
+    T* mirror;  // LaunchCtx::mirror (fused halo exchange), or nullptr
+    long long mshift;
     T w[27];
 };
 
@@ -192,7 +194,11 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
             T* o = out + a.origin + (long long)po * a.pitch0 + (long long)(gy + y) * a.pitch1 +
                    (gx + x);
 #pragma unroll
-            for (int cy = 0; cy < VY; ++cy) store_row<T, VX>(o + cy * a.pitch1, accB[cy], ok[cy]);
+            for (int cy = 0; cy < VY; ++cy) {
+                store_row<T, VX>(o + cy * a.pitch1, accB[cy], ok[cy]);
+                if (a.mirror)
+                    store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, accB[cy], ok[cy]);
+            }
         }
         // output q continues (di = 0), output q+1 starts (di = -1)
         apply9<EXACT, false>(a.w + 9, nb, accA);
@@ -379,6 +385,7 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) v[cx] = fix_zero<EXACT>(a2B[cy][cx]);
                 store_row<T, VX>(o + cy * a.pitch1, v, cout[cy]);
+                if (a.mirror) store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, v, cout[cy]);
             }
         }
         apply9<EXACT, false>(a.w + 9, nb2, a2A);
@@ -416,6 +423,8 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     a.pitch0 = g.pitch[0];
     a.pitch1 = g.pitch[1];
     a.origin = g.origin;
+    a.mirror = static_cast<T*>(c.mirror);
+    a.mshift = c.mirror_shift;
     for (int q = 0; q < 27; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     constexpr int bytes = smem_bytes<T>();
     int per_sm = 1, nsm = 148;
@@ -452,6 +461,8 @@ Status launch2(const LaunchCtx& c, const void* in, void* out) {
     a.pitch0 = g.pitch[0];
     a.pitch1 = g.pitch[1];
     a.origin = g.origin;
+    a.mirror = static_cast<T*>(c.mirror);
+    a.mshift = c.mirror_shift;
     for (int q = 0; q < 27; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     constexpr int bytes = smem2_bytes<T>();
     int per_sm = 1, nsm = 148;

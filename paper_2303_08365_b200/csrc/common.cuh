@@ -173,6 +173,11 @@ struct LaunchCtx {
     // restricted, so interior and seam planes can be launched separately.
     int64_t lo0 = 0;
     int64_t hi0 = INT64_MAX;
+    // Fused halo exchange: every value stored to `out` is also stored to
+    // `mirror` at the same element index + mirror_shift (a neighbour slab's
+    // ghost planes in peer memory, same layout).  nullptr = no mirror.
+    void* mirror = nullptr;
+    int64_t mirror_shift = 0;
 
     int64_t range_lo() const { return lo0; }
     int64_t range_hi() const { return std::min<int64_t>(hi0, g->n[3 - g->dims]); }

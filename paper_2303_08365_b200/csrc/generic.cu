@@ -16,6 +16,8 @@ struct GenericArgs {
     int64_t n[3];  // box extents (normalised)
     int64_t base;  // element index of box corner
     int64_t pitch0, pitch1;
+    T* mirror;  // LaunchCtx::mirror (fused halo exchange), or nullptr
+    int64_t mshift;
     int ntaps;
     int32_t delta[MAXT];
     T w[MAXT];
@@ -38,6 +40,7 @@ __global__ void __launch_bounds__(256) generic_sweep_kernel(const T* __restrict_
 #pragma unroll 4
         for (int t = 1; t < a.ntaps; ++t) acc = madd<EXACT>(acc, a.w[t], in[idx + a.delta[t]]);
         out[idx] = acc;
+        if (a.mirror) a.mirror[idx + a.mshift] = acc;
     }
 }
 
@@ -50,6 +53,8 @@ Status launch(const LaunchCtx& c, const void* in, void* out, const int64_t lo[3]
     a.base = g.origin + lo[0] * g.pitch[0] + lo[1] * g.pitch[1] + lo[2];
     a.pitch0 = g.pitch[0];
     a.pitch1 = g.pitch[1];
+    a.mirror = static_cast<T*>(c.mirror);
+    a.mshift = c.mirror_shift;
     a.ntaps = c.taps->ntaps;
     for (int t = 0; t < a.ntaps; ++t) {
         const int* o = c.taps->off[t];

@@ -36,6 +36,8 @@ struct S2Args {
     int64_t wout;            // output columns per strip
     int64_t hl;              // left margin of the strip (>= R*K, vector aligned)
     int64_t total_warps;
+    T* mirror;  // LaunchCtx::mirror (fused halo exchange), or nullptr
+    int64_t mshift;
     T w[25];
 };
 
@@ -79,6 +81,29 @@ __device__ __forceinline__ void load_row(const T* __restrict__ p, bool ok, T (&v
     } else {
 #pragma unroll
         for (int i = 0; i < V; ++i) v[i] = T(0);
+    }
+}
+
+// One lane's V outputs of a row: a vector store when the whole run is in the
+// output strip, predicated scalars otherwise.
+template <typename T, int V>
+__device__ __forceinline__ void store_vals(T* dst, const T (&res)[V], const bool (&cout)[V],
+                                           bool all_out) {
+    if (all_out) {
+        if constexpr (sizeof(T) * V == 16) {
+            typename Vec<T, V>::type o;
+            T* os = reinterpret_cast<T*>(&o);
+#pragma unroll
+            for (int v = 0; v < V; ++v) os[v] = res[v];
+            *reinterpret_cast<typename Vec<T, V>::type*>(dst) = o;
+        } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) dst[v] = res[v];
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (cout[v]) dst[v] = res[v];
     }
 }
 
@@ -195,22 +220,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
 #pragma unroll
                 for (int v = 0; v < V; ++v) res[v] = fix_zero<EXACT>(res[v]);
                 T* dst = base_out + x * a.pitch;
-                if (all_out) {
-                    if constexpr (sizeof(T) * V == 16) {
-                        typename Vec<T, V>::type o;
-                        T* os = reinterpret_cast<T*>(&o);
-#pragma unroll
-                        for (int v = 0; v < V; ++v) os[v] = res[v];
-                        *reinterpret_cast<typename Vec<T, V>::type*>(dst) = o;
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < V; ++v) dst[v] = res[v];
-                    }
-                } else {
-#pragma unroll
-                    for (int v = 0; v < V; ++v)
-                        if (cout[v]) dst[v] = res[v];
-                }
+                store_vals<T, V>(dst, res, cout, all_out);
+                if (a.mirror) store_vals<T, V>(a.mirror + (dst - out) + a.mshift, res, cout, all_out);
             }
         }
     };
@@ -265,6 +276,8 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.hrow = g.h[1];
     a.pitch = g.pitch[1];
     a.origin = g.origin;
+    a.mirror = static_cast<T*>(c.mirror);
+    a.mshift = c.mirror_shift;
     a.col_lo = -g.off2;
     a.col_hi = g.pitch[1] - g.off2;
     constexpr int vec = 16 / sizeof(T);

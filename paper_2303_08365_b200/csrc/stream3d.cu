@@ -22,6 +22,8 @@ struct Star3Args {
     int64_t origin;
     int64_t chunk;  // a0 planes per CTA
     int64_t lo0, hi0;  // output planes [lo0, hi0) of a0
+    T* mirror;  // LaunchCtx::mirror (fused halo exchange), or nullptr
+    int64_t mshift;
     T w[7];
 };
 
@@ -48,6 +50,7 @@ __global__ void __launch_bounds__(kBX* kBY) star3d_r1_kernel(const T* __restrict
         acc = madd<EXACT>(acc, a.w[5], __ldg(in + p + P1));
         acc = madd<EXACT>(acc, a.w[6], next);
         out[p] = acc;
+        if (a.mirror) a.mirror[p + a.mshift] = acc;
         prev = cur;
         cur = next;
         p += P0;
@@ -71,6 +74,8 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     a.pitch0 = g.pitch[0];
     a.pitch1 = g.pitch[1];
     a.origin = g.origin;
+    a.mirror = static_cast<T*>(c.mirror);
+    a.mshift = c.mirror_shift;
     for (int t = 0; t < 7; ++t) a.w[t] = static_cast<T>(c.taps->w[t]);
     const int64_t gx = (g.n[2] + kBX - 1) / kBX, gy = (g.n[1] + kBY - 1) / kBY;
     // Enough CTAs for ~8 resident per SM, but chunks of >= 32 planes.

@@ -105,6 +105,8 @@ struct TbArgs {
     int lo0, hi0;  // output planes [lo0, hi0) of a0
     int h0, h1, off2;
     long long pitch0, pitch1, origin;
+    T* mirror;  // LaunchCtx::mirror (fused halo exchange), or nullptr
+    long long mshift;
     T w[7];
 };
 
@@ -231,6 +233,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) v[cx] = fix_zero<EXACT>(res[cy][cx]);
                 store_row<T, VX>(o + cy * a.pitch1, v, cout[cy]);
+                if (a.mirror) store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, v, cout[cy]);
             }
         }
     }
@@ -410,6 +413,8 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.pitch0 = g.pitch[0];
     a.pitch1 = g.pitch[1];
     a.origin = g.origin;
+    a.mirror = static_cast<T*>(c.mirror);
+    a.mshift = c.mirror_shift;
     for (int q = 0; q < 7; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     const long long nchunks = (span + a.chunk - 1) / a.chunk;
     const unsigned grid = (unsigned)(tiles * nchunks);

@@ -92,21 +92,25 @@ class DeviceGrid:
 
     def sweep_range(self, kernel: StencilKernel, lo: int, hi: int, steps: int, *,
                     fused_steps: int = 0, mode: str = "exact", engine: str = "auto",
-                    stream=None) -> int:
+                    mirror: int = 0, mirror_planes: int = 0, stream=None) -> int:
         """One fused pass of `steps` time steps from the current buffer into
         the other one, storing only the planes [lo, hi) of axis 0
         (tsr_sweep_range).  Does not flip the buffers: a slab round launches
         its interior and seam ranges separately, then calls ``flip``.
+        With `mirror` (a device address, e.g. a peer slab's next buffer
+        mapped by CUDA IPC) every stored plane p is also written to plane
+        p + mirror_planes of that buffer (tsr_sweep_range_mirror).
         Returns the number of kernels launched (0 for an empty range)."""
         if hi <= lo:
             return 0
         L = _abi.lib()
         opts = _abi.make_opts(fused_steps, mode, engine)
         with self.torch.cuda.device(self.device):
-            _abi.check(L.tsr_sweep_range(ctypes.byref(kernel.c_struct()), ctypes.byref(self.desc),
-                                         ctypes.byref(self.layout), self.ptr(self.cur),
-                                         self.ptr(1 - self.cur), int(lo), int(hi), int(steps),
-                                         ctypes.byref(opts), self._stream(stream)))
+            _abi.check(L.tsr_sweep_range_mirror(
+                ctypes.byref(kernel.c_struct()), ctypes.byref(self.desc),
+                ctypes.byref(self.layout), self.ptr(self.cur), self.ptr(1 - self.cur), int(lo),
+                int(hi), int(steps), ctypes.byref(opts), ctypes.c_void_p(mirror or None),
+                int(mirror_planes), self._stream(stream)))
         return 1
 
     def flip(self, steps: int) -> None:

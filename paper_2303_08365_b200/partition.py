@@ -24,6 +24,14 @@ CPU+GPU ratio split is out of scope per the north star):
   "compute interior of step 0 -> recv and install ghost -> finish seam"
   ordering of HaloWorker::run_round, scheduler.cpp:371-406).
 
+* transport="peer" (the B200 path, north star tier 3 over NVLink): no
+  message at all.  Neighbour slabs map each other's buffers with CUDA IPC;
+  the seam pass of round n stores its planes both locally and straight into
+  the neighbours' next-buffer ghost planes (tsr_sweep_range_mirror: the
+  compute and the transfer are one kernel), then bumps a round flag in the
+  neighbours' memory; before its own seam pass a rank waits on its flags
+  (tsr_peer_wait).  The interior pass never waits.  See PeerLink.
+
 Seam-side halo planes of a local slab are beyond the ghost region and never
 influence owned rows; ``poison=True`` fills them with NaN to prove it (the
 reference's run_heterogeneous_instrumented, scheduler.cpp:410-421).
@@ -168,9 +176,9 @@ class _DeviceState:
         self._ev_comm.record(self._xs)
         torch.cuda.current_stream(self.dg.device).wait_event(self._ev_comm)
 
-    def sweep_range(self, lo, hi, n):
+    def sweep_range(self, lo, hi, n, mirror=0, mirror_planes=0):
         return self.dg.sweep_range(self.kernel, lo, hi, n, fused_steps=self.fused_steps,
-                                   mode=self.mode)
+                                   mode=self.mode, mirror=mirror, mirror_planes=mirror_planes)
 
     def flip(self, n):
         self.dg.flip(n)
@@ -235,13 +243,114 @@ class _HostState:
         self.g.flip_parity()
 
 
+class PeerLink:
+    """CUDA-IPC mappings of the neighbour slabs' two buffers and round flags
+    (csrc/peer.cu).  Collective constructor: every rank of `group` calls it.
+
+    flags[0] / flags[1] of a rank count the rounds its lo / hi neighbour has
+    completed; a rank signals round completion into its lo neighbour's
+    flags[1] and its hi neighbour's flags[0]."""
+
+    def __init__(self, plan: SlabPlan, dg, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import _abi
+        self._abi = _abi
+        self.dist, self.group = dist, group
+        self.torch = torch
+        self.dg = dg
+        self.flags = torch.zeros(2, dtype=torch.int32, device=dg.device)
+        torch.cuda.synchronize(dg.device)
+        mine = {"rank": plan.rank, "buf": [_abi.ipc_export(dg.ptr(0)), _abi.ipc_export(dg.ptr(1))],
+                "flags": _abi.ipc_export(self.flags.data_ptr())}
+        info = [None] * plan.world
+        dist.all_gather_object(info, mine, group=group)
+        self._bases = {}
+        self.peer = {}
+        err = None
+        try:
+            for side, nb in (("lo", plan.rank - 1), ("hi", plan.rank + 1)):
+                if not 0 <= nb < plan.world:
+                    continue
+                peer = info[nb]
+                nplan = plan_slabs(plan.global_extent, plan.radius, plan.fused_steps, plan.world,
+                                   nb, plan.halo)
+                if side == "lo":  # my first own planes -> its ghost_hi planes
+                    shift = (nplan.ghost_lo + nplan.own) - plan.ghost_lo
+                    word = 1
+                else:             # my last own planes -> its ghost_lo planes (rows 0..d)
+                    shift = -(plan.ghost_lo + plan.own - plan.depth)
+                    word = 0
+                self.peer[side] = {"buf": [self._map(*peer["buf"][0]),
+                                           self._map(*peer["buf"][1])],
+                                   "flag": self._map(*peer["flags"]) + 4 * word,
+                                   "shift": shift}
+        except Exception as e:  # noqa: BLE001 - reported collectively below
+            err = f"rank {plan.rank}: {e}"
+        errs = [None] * plan.world
+        dist.all_gather_object(errs, err, group=group)
+        failed = [e for e in errs if e]
+        if failed:  # every rank gives up together (no rank left waiting on a flag)
+            for base in self._bases.values():
+                self._abi.ipc_close(base)
+            self._bases, self.peer = {}, {}
+            raise RuntimeError("peer mapping failed: " + "; ".join(failed))
+        dist.barrier(group=group)
+
+    def _map(self, handle: bytes, offset: int) -> int:
+        if handle not in self._bases:
+            self._bases[handle] = self._abi.ipc_open(handle)
+        return self._bases[handle] + offset
+
+    def _stream(self) -> int:
+        return self.torch.cuda.current_stream(self.dg.device).cuda_stream
+
+    def wait(self, rounds_done: int) -> int:
+        """Later work on the current stream waits until both neighbours have
+        completed `rounds_done` rounds.  Returns the kernels launched."""
+        L, n = self._abi.lib(), 0
+        for side, word in (("lo", 0), ("hi", 1)):
+            if side in self.peer:
+                self._abi.check(L.tsr_peer_wait(self.flags.data_ptr() + 4 * word,
+                                                rounds_done & 0xffffffff, self._stream()))
+                n += 1
+        return n
+
+    def signal(self, rounds_done: int) -> int:
+        L, n = self._abi.lib(), 0
+        for side in ("lo", "hi"):
+            if side in self.peer:
+                self._abi.check(L.tsr_peer_signal(self.peer[side]["flag"],
+                                                  rounds_done & 0xffffffff, self._stream()))
+                n += 1
+        return n
+
+    def mirror(self, side: str, which: int) -> tuple[int, int]:
+        """(address of the neighbour's buffer `which`, plane shift) for a seam
+        pass on `side`."""
+        p = self.peer[side]
+        return p["buf"][which], p["shift"]
+
+    def close(self) -> None:
+        """Collective: no rank unmaps before every rank's stores have landed."""
+        self.torch.cuda.synchronize(self.dg.device)
+        self.dist.barrier(group=self.group)
+        for base in self._bases.values():
+            self._abi.ipc_close(base)
+        self._bases = {}
+        self.peer = {}
+
+
 class SlabRunner:
     """Round driver for one rank (HaloWorker::run_round generalised to P
     slabs).  ``advance(n)`` runs one round of n <= k steps: exchange the
     ghost planes with both neighbours, then n fused steps on the local slab."""
 
-    def __init__(self, plan: SlabPlan, state, group=None, overlap: bool = True):
+    def __init__(self, plan: SlabPlan, state, group=None, overlap: bool = True,
+                 transport: str = "nccl"):
         import torch.distributed as dist
+        if transport not in ("nccl", "peer"):
+            raise ValueError("transport must be 'nccl' or 'peer'")
         self.dist = dist
         # gloo cannot move CUDA tensors point-to-point: stage through host
         # memory (tests run several ranks on one GPU this way); NCCL sends
@@ -256,17 +365,26 @@ class SlabRunner:
         self.round = 0
         self.log = CommLog()
         self.exchange_bytes = 0
+        self.transport = transport
+        self.link = None
+        if transport == "peer" and plan.world > 1:
+            if not isinstance(state, _DeviceState):
+                raise ValueError("the peer transport needs device slabs")
+            # ghosts consistent before the first round (one message exchange,
+            # outside any timed region), then IPC mappings for the rounds
+            self.exchange()
+            self.link = PeerLink(plan, state.dg, group)
 
     # -- constructors -----------------------------------------------------
     @classmethod
     def on_device(cls, ts, kernel, plan: SlabPlan, host_local, device, mode="exact",
-                  group=None, overlap=True):
+                  group=None, overlap=True, transport="nccl"):
         return cls(plan, _DeviceState(ts, kernel, host_local, device, plan.fused_steps, mode),
-                   group, overlap)
+                   group, overlap, transport)
 
     @classmethod
     def synthetic(cls, ts, kernel, plan: SlabPlan, dtype, device, seed=1, fused_steps=None,
-                  mode="exact", group=None, overlap=True):
+                  mode="exact", group=None, overlap=True, transport="nccl"):
         """Benchmark slab: the local grid is filled with fill_random(seed)
         directly (no global host grid); the first exchange makes the ghost
         planes consistent with the neighbours."""
@@ -281,7 +399,7 @@ class SlabRunner:
                               plan.halo, esize)
         host = cls_(plan.local_extent, plan.halo)
         ts.fill_random(host, seed)
-        return cls.on_device(ts, kernel, plan, host, device, mode, group, overlap)
+        return cls.on_device(ts, kernel, plan, host, device, mode, group, overlap, transport)
 
     @classmethod
     def on_host(cls, plan: SlabPlan, host_local, step_fn, group=None, overlap=False):
@@ -321,17 +439,59 @@ class SlabRunner:
         for _, t in sends:
             self.exchange_bytes += t.numel() * t.element_size()
 
-    def ranges(self, n: int):
+    def ranges(self, n: int, depth: int = 0):
         """(interior, seams) plane ranges of one overlapped round in local
         interior coordinates: the interior's n-step cone stays inside the
-        owned planes; the seams need the ghosts."""
+        owned planes; the seams need the ghosts.  `depth` widens the seams
+        to that many planes (the peer transport's seams are the planes the
+        neighbours' ghosts receive: always the full r*k)."""
         p = self.plan
-        dl = p.radius * n if p.ghost_lo else 0
-        dh = p.radius * n if p.ghost_hi else 0
+        d = max(p.radius * n, depth)
+        dl = d if p.ghost_lo else 0
+        dh = d if p.ghost_hi else 0
         lo, hi = p.ghost_lo, p.ghost_lo + p.own
         if hi - lo <= dl + dh:
             return (lo, lo), [(lo, hi)]
         return (lo + dl, hi - dh), [(lo, lo + dl), (hi - dh, hi)]
+
+    def _round_peer(self, n: int):
+        """One round over peer memory: interior pass (no wait), wait for the
+        neighbours' previous round, seam passes that also store into the
+        neighbours' ghost planes, signal."""
+        st, link, p = self.state, self.link, self.plan
+        (ilo, ihi), seams = self.ranges(n, depth=p.depth)
+        launches = st.sweep_range(ilo, ihi, n)
+        launches += link.wait(self.round)
+        nxt = 1 - st.dg.cur
+        first, last = p.ghost_lo, p.ghost_lo + p.own
+        # the depth planes each neighbour's ghosts receive
+        mirrored = []
+        if "lo" in link.peer:
+            mirrored.append(("lo", first, min(last, first + p.depth)))
+        if "hi" in link.peer:
+            mirrored.append(("hi", max(first, last - p.depth), last))
+        # seam planes no mirrored pass covers (only in a slab thinner than 2
+        # seams plus the interior cone): plain passes
+        for lo, hi in seams:
+            for _, a, b in mirrored:
+                if a <= lo < b:
+                    lo = b
+                if a < hi <= b:
+                    hi = a
+            if hi > lo:
+                launches += st.sweep_range(lo, hi, n)
+        for side, a, b in mirrored:
+            addr, shift = link.mirror(side, nxt)
+            launches += st.sweep_range(a, b, n, mirror=addr, mirror_planes=shift)
+            self.exchange_bytes += p.bytes_per_message
+            self.log.records.append(CommRecord(self.round, f"r{p.rank}_to_{side}",
+                                               p.bytes_per_message))
+        launches += link.signal(self.round + 1)
+        st.flip(n)
+
+        class _S:
+            kernel_launches = launches
+        return _S()
 
     def _round_overlapped(self, n: int):
         """HaloWorker::run_round's order (scheduler.cpp:371-406) on two
@@ -354,7 +514,9 @@ class SlabRunner:
     def advance(self, n: int):
         if n > self.fused_steps:
             raise ValueError("a round advances at most k = depth / r steps")
-        if self.plan.world > 1 and self.overlap:
+        if self.link is not None:
+            st = self._round_peer(n)
+        elif self.plan.world > 1 and self.overlap:
             st = self._round_overlapped(n)
         else:
             if self.plan.world > 1:
@@ -387,8 +549,15 @@ class SlabRunner:
         h0 = g.halo[0]
         return g.padded(g.parity)[h0 + self.plan.ghost_lo:h0 + self.plan.ghost_lo + self.plan.own]
 
+    def close(self) -> None:
+        """Collective teardown of the peer mappings (no-op for NCCL)."""
+        if self.link is not None:
+            self.link.close()
+            self.link = None
+
     def comm_summary(self) -> dict:
-        return {"rounds": self.round, "overlap": bool(self.overlap and self.plan.world > 1),
+        return {"rounds": self.round, "transport": self.transport if self.plan.world > 1 else None,
+                "overlap": bool(self.overlap and self.plan.world > 1),
                 "messages_sent": len(self.log.records),
                 "bytes_per_message": self.plan.bytes_per_message,
                 "halo_depth": self.plan.depth, "fused_steps": self.fused_steps,

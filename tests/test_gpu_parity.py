@@ -290,3 +290,61 @@ def test_sweep_range_stores_only_its_planes(ts, orc, name, extent, fused, dt):
         dg.sweep_range(k, 0, n0 + 1, fused, fused_steps=fused)
     with pytest.raises(ValueError):
         dg.sweep_range(k, 0, n0, fused + 1, fused_steps=fused)
+
+
+@pytest.mark.parametrize("name,extent,fused,dt", [
+    ("Heat-3D", [40, 36, 70], 3, "f64"),     # tb3d
+    ("Box-3D27P", [30, 30, 50], 1, "f32"),   # box3d
+    ("Box-3D27P", [30, 30, 50], 2, "f64"),   # box3d two-level
+    ("Box-2D9P", [120, 150], 4, "f64"),     # stream2d
+    ("Heat-1D", [300], 1, "f64"),           # generic
+])
+def test_sweep_range_mirror(ts, orc, name, extent, fused, dt):
+    """tsr_sweep_range_mirror (the fused halo exchange): the stored planes
+    land both in `out` and, shifted by `mirror_planes`, in the mirror buffer
+    (here a second buffer on the same device); nothing else of the mirror is
+    touched."""
+    import torch
+    k = ts.find_benchmark(name).kernel
+    g = random_grid(ts, orc, extent, [k.radius] * k.dims, 5, dt)
+    ref = g.copy()
+    orc.naive_run(ref, k, fused)
+    want = ref.interior_view(ref.parity)
+    n0 = extent[0]
+    lo, hi, shift = n0 - 3 * k.radius, n0, -(n0 - 3 * k.radius)  # last planes -> first planes
+    dg = ts.DeviceGrid(g, torch.device("cuda", 0))
+    mirror = ts.DeviceGrid(g, torch.device("cuda", 0), upload=False)
+    mirror.buf[0].fill_(float("nan"))
+    dg.sweep_range(k, lo, hi, fused, fused_steps=fused, mirror=mirror.ptr(0), mirror_planes=shift)
+    dg.flip(fused)
+    got = g.copy()
+    dg.download(got)
+    assert got.interior_view(got.parity)[lo:hi].tobytes() == want[lo:hi].tobytes()
+    m = g.copy()
+    mirror.cur, mirror.steps_done = 0, 0
+    mirror.download(m)
+    mi = m.interior_view(m.parity)
+    assert mi[:hi - lo].tobytes() == want[lo:hi].tobytes()
+    assert np.isnan(mi[hi - lo:]).all()
+    with pytest.raises(ValueError):  # mirror aliasing the output buffer
+        dg.sweep_range(k, lo, hi, fused, fused_steps=fused, mirror=dg.ptr(1 - dg.cur))
+
+
+def test_peer_flags_order_a_stream(ts):
+    """tsr_peer_signal / tsr_peer_wait on one stream: the wait kernel passes
+    once the word reaches the value (wrap-around compare), and work queued
+    behind it runs after it."""
+    import ctypes
+    import torch
+    from paper_2303_08365_b200 import _abi
+    L = _abi.lib()
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    _abi.check(L.tsr_peer_signal(ctypes.c_void_p(flag.data_ptr()), 7, s))
+    _abi.check(L.tsr_peer_wait(ctypes.c_void_p(flag.data_ptr()), 7, s))
+    _abi.check(L.tsr_peer_wait(ctypes.c_void_p(flag.data_ptr()), 0xfffffff0, s))  # 7 is "after" it
+    flag.add_(1)
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 8
+    h, off = _abi.ipc_export(flag.data_ptr())
+    assert len(h) == 64 and off >= 0

@@ -96,7 +96,7 @@ def test_reference_message_and_ghost_counts(ts, orc, tmp_path):
         plan_slabs([8, 8], 1, 5, 2, 0)  # subdomain smaller than the halo depth
 
 
-def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, overlap):
+def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, mode):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -113,8 +113,11 @@ def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, overlap):
     orc.fill_random(glob, 500)
     plan = plan_slabs(extent, kern.radius, k, world, rank)
     loc = local_from_global(glob, plan, poison=True)
-    runner = SlabRunner.on_device(ts, kern, plan, loc, torch.device("cuda", 0), overlap=overlap)
+    runner = SlabRunner.on_device(ts, kern, plan, loc, torch.device("cuda", 0),
+                                  overlap=mode != "serial",
+                                  transport="peer" if mode == "peer" else "nccl")
     runner.run(steps)
+    runner.close()  # peer transport: every neighbour's stores have landed
     np.save(os.path.join(out_dir, f"own{rank}.npy"), runner.own_rows(loc))
     np.save(os.path.join(out_dir, f"log{rank}.npy"),
             np.array([len(runner.log.records), runner.round, runner.log.ghost_recompute_points]))
@@ -123,7 +126,7 @@ def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, overlap):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("overlap", [False, True], ids=["serial", "overlap"])
+@pytest.mark.parametrize("mode", ["serial", "overlap", "peer"])
 @pytest.mark.parametrize("world,name,extent,steps,k", [
     (2, "Heat-3D", [70, 40, 67], 7, 3),   # tb3d engine on each slab
     (3, "Box-2D9P", [90, 130], 9, 4),    # stream2d engine
@@ -131,14 +134,15 @@ def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, overlap):
     (2, "Box-3D27P", [44, 30, 50], 5, 2),  # box3d two-level engine
     (3, "Heat-1D", [300], 6, 1),          # generic engine, 1-D slabs
 ])
-def test_slabs_on_device_equal_oracle(ts, orc, tmp_path, world, name, extent, steps, k,
-                                      overlap):
+def test_slabs_on_device_equal_oracle(ts, orc, tmp_path, world, name, extent, steps, k, mode):
     """The device slab state (pitched HBM buffers, tsr_advance or
     tsr_sweep_range on two streams, zero-copy plane views) with several ranks
-    sharing one GPU over gloo."""
+    sharing one GPU over gloo; `peer`: the seam passes store straight into the
+    neighbour processes' ghost planes through CUDA IPC mappings and the
+    rounds are ordered by device-side flags (no message on the data path)."""
     port = _free_port()
     mp.start_processes(_gpu_worker, args=(world, port, name, extent, steps, k, str(tmp_path),
-                                          overlap),
+                                          mode),
                        nprocs=world, join=True, start_method="spawn")
     kern = ts.find_benchmark(name).kernel
     ref = ts.Grid(extent, [kern.radius] * len(extent))
