@@ -1,8 +1,11 @@
 // tb3d.cu — 3-D radius-1 star (7-point) sweep with K time steps fused per
 // HBM pass: the paper's three tiers rebuilt for sm_100a.
 //
-//  * Memory tier: each CTA owns an output tile of (32-2(K-1)) x (64-2(K-1))
-//    cells of the (a1, a2) plane and streams a chunk of a0 planes.  Level-0
+//  * Memory tier: a CTA owns an output tile of (32-2(K-1)) x (64-2(K-1))
+//    cells of the (a1, a2) plane and streams consecutive a0 planes of it;
+//    for K >= 2 the grid is persistent (one CTA per SM, each an equal share
+//    of the (tile, plane) positions, so the wavefront refills only when a
+//    CTA moves to its next tile).  Level-0
 //    planes (the tile plus a (K-1)+1 halo ring) arrive by TMA
 //    (cp.async.bulk.tensor.3d) into a 5-stage shared-memory ring guarded by
 //    mbarriers (planes t-2 .. t+2 of step t).
@@ -101,7 +104,8 @@ template <typename T>
 struct TbArgs {
     int n0, n1, n2;
     int tiles_x, tiles_y;
-    int chunk;
+    long long per_cta;  // (tile, plane) positions per CTA (persistent schedule), or
+    int chunk;          // > 0: one chunk of a0 planes per CTA, tiles fastest
     int lo0, hi0;  // output planes [lo0, hi0) of a0
     int h0, h1, off2;
     long long pitch0, pitch1, origin;
@@ -142,8 +146,8 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 // were written (3-deep SMEM buffers, one __syncthreads per step).
 template <typename T, int K, bool EXACT, int PH, bool SEL, typename G, bool EARLY0>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
-                                          uint64_t* bar, int it, int t_begin, int i0, int i1,
-                                          int lx, int x, int y, int gx, int gy,
+                                          uint64_t* bar, unsigned gbase, int it, int t_begin,
+                                          int i0, int i1, int lx, int x, int y, int gx, int gy,
                                           const bool (&cint)[G::VY][VX],
                                           const bool (&cout)[G::VY][VX],
                                           T (&Hs)[K][3][G::VY][VX]) {
@@ -153,11 +157,12 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
     constexpr int LEV = lev_bytes<T, G>() / (int)sizeof(T);
     constexpr int BX = BX0<T>, PL = PADL<T>;
     const int t = t_begin + it;
-    const int slot = it % STAGES;
+    const unsigned gi = gbase + it;  // ring loads since kernel start: slot and phase
+    const int slot = gi % STAGES;
     const T* P0 = ring + slot * SLOT;
     P2 early[VY];
     if constexpr (EARLY0) {  // level-0 rows of plane t fetched before the levels' math
-        mbar_wait(&bar[slot], (it / STAGES) & 1);
+        mbar_wait(&bar[slot], (gi / STAGES) & 1);
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
             early[cy] = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
@@ -173,7 +178,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
         P2 u, d;
         const T* Pm = nullptr;
         if (l == 1) {
-            Pm = ring + ((it - 2 + 2 * STAGES) % STAGES) * SLOT;  // level 0, plane t-2
+            Pm = ring + ((gi + 2 * STAGES - 2) % STAGES) * SLOT;  // level 0, plane t-2
             u = *reinterpret_cast<const P2*>(Pm + (y) * BX + x + PL);
             d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX + x + PL);
         } else {
@@ -238,7 +243,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
         }
     }
     // Level 0 last: plane t into the window slot level 1 has just consumed.
-    if constexpr (!EARLY0) mbar_wait(&bar[slot], (it / STAGES) & 1);
+    if constexpr (!EARLY0) mbar_wait(&bar[slot], (gi / STAGES) & 1);
 #pragma unroll
     for (int cy = 0; cy < VY; ++cy) {
         const P2 v = EARLY0 ? early[cy]
@@ -262,33 +267,11 @@ __global__ void __launch_bounds__(G::NT, 1)
 
     const int tid = threadIdx.x;
     const int lx = tid & 31, ly = tid >> 5;
-    const int tile = blockIdx.x;
-    const int bx = tile % a.tiles_x;
-    const int by = (tile / a.tiles_x) % a.tiles_y;
-    const int bz = tile / (a.tiles_x * a.tiles_y);
     constexpr int TX = TXO<T, K>, TY = R1Y - 2 * (K - 1);
     constexpr int PL = PADL<T>, HX = HXL<T, K>;
-    const int gx = bx * TX - HX;       // global a2 of region-1 column 0
-    const int gy = by * TY - (K - 1);  // global a1 of region-1 row 0
-    const int i0 = a.lo0 + bz * a.chunk;
-    const int i1 = min(i0 + a.chunk, a.hi0);
-    // level-0 planes i0-K .. i1+K-1; level K finishes plane i1-1 at step i1-1+2K
-    const int t_begin = i0 - K, t_end = i1 + 2 * K;
-    const int niter = t_end - t_begin;
-    const int nload = i1 - i0 + 2 * K;  // level-0 planes actually needed
-
+    constexpr unsigned kBoxBytes = BX0<T> * BY0 * sizeof(T);
     // Columns owned: region-1 (y, x) = (VY*ly + cy, VX*lx + cx).
     const int x = VX * lx, y = VY * ly;
-    bool cint[VY][VX], cout[VY][VX];
-#pragma unroll
-    for (int cy = 0; cy < VY; ++cy)
-#pragma unroll
-        for (int cx = 0; cx < VX; ++cx) {
-            const int ga1 = gy + y + cy, ga2 = gx + x + cx;
-            cint[cy][cx] = ga1 >= 0 && ga1 < a.n1 && ga2 >= 0 && ga2 < a.n2;
-            cout[cy][cx] = cint[cy][cx] && y + cy >= K - 1 && y + cy < R1Y - (K - 1) &&
-                           x + cx >= HX && x + cx < HX + TX;
-        }
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
@@ -296,21 +279,29 @@ __global__ void __launch_bounds__(G::NT, 1)
         prefetch_tmap(&tmap);
     }
     __syncthreads();
-    constexpr unsigned kBoxBytes = BX0<T> * BY0 * sizeof(T);
-    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned box start
-    // plane index j (0-based from t_begin) is loaded at most once; the steps
-    // that drain the wavefront past the last needed plane (i1+K-1) re-load
-    // that plane instead, so a launch never reads outside its dependency cone
-    // (a slab's interior range runs while its ghost planes are being written)
-    const int last_plane = a.h0 + t_begin + nload - 1;
-    if (tid == 0) {
-        for (int s = 0; s < STAGES && s < niter; ++s) {
-            mbar_expect_tx(&bar[s], kBoxBytes);
-            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1,
-                        min(a.h0 + t_begin + s, last_plane));
-        }
-    }
 
+    // Persistent schedule: the CTA owns positions [pos, end) of the
+    // (tile, plane) space, tile-major, and streams them as segments of
+    // consecutive planes of one tile; only a tile change refills the
+    // wavefront (3K steps), instead of every chunk of a one-chunk-per-CTA
+    // grid.
+    // K = 1 is HBM-bound: it keeps one chunk per CTA with the tiles of a
+    // chunk on consecutive CTAs, so neighbouring tiles read their shared
+    // halo rows at the same time and L2 serves the second read.
+    const long long span = a.hi0 - a.lo0;
+    const long long total = (long long)a.tiles_x * a.tiles_y * span;
+    long long pos, end;
+    if (a.chunk > 0) {
+        const int ntile = a.tiles_x * a.tiles_y;
+        const int tile = blockIdx.x % ntile, bz = blockIdx.x / ntile;
+        const long long off = (long long)bz * a.chunk;
+        pos = (long long)tile * span + off;
+        end = pos + min((long long)a.chunk, span - off);
+    } else {
+        pos = (long long)blockIdx.x * a.per_cta;
+        end = min(pos + a.per_cta, total);
+    }
+    unsigned gbase = 0;  // ring loads issued by earlier segments
     T Hs[K][3][VY][VX];
 #pragma unroll
     for (int l = 0; l < K; ++l)
@@ -321,52 +312,97 @@ __global__ void __launch_bounds__(G::NT, 1)
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) Hs[l][s][cy][cx] = T(0);
 
-    auto after = [&](int it) {
-        __syncthreads();
-        // Plane t-2 was last read in this step (level-1 neighbours): its slot
-        // takes plane t-2+STAGES.
-        if (tid == 0 && it >= 2 && it - 2 + STAGES < niter) {
-            const int s = (it - 2) % STAGES;
+    while (pos < end) {
+        const int tile = (int)(pos / span);
+        const int i0 = a.lo0 + (int)(pos - (long long)tile * span);
+        const int i1 = (int)min((long long)a.hi0, (long long)i0 + (end - pos));
+        pos += i1 - i0;
+        const int bx = tile % a.tiles_x;
+        const int by = tile / a.tiles_x;
+        const int gx = bx * TX - HX;       // global a2 of region-1 column 0
+        const int gy = by * TY - (K - 1);  // global a1 of region-1 row 0
+        // level-0 planes i0-K .. i1+K-1; level K finishes plane i1-1 at step i1-1+2K
+        const int t_begin = i0 - K, t_end = i1 + 2 * K;
+        const int niter = t_end - t_begin;
+        const int nload = i1 - i0 + 2 * K;  // level-0 planes actually needed
+
+        bool cint[VY][VX], cout[VY][VX];
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < VX; ++cx) {
+                const int ga1 = gy + y + cy, ga2 = gx + x + cx;
+                cint[cy][cx] = ga1 >= 0 && ga1 < a.n1 && ga2 >= 0 && ga2 < a.n2;
+                cout[cy][cx] = cint[cy][cx] && y + cy >= K - 1 && y + cy < R1Y - (K - 1) &&
+                               x + cx >= HX && x + cx < HX + TX;
+            }
+
+        const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned box start
+        // plane index j (0-based from t_begin) is loaded at most once; the
+        // steps that drain the wavefront past the last needed plane (i1+K-1)
+        // re-load that plane instead, so a launch never reads outside its
+        // dependency cone (a slab's interior range runs while its ghost
+        // planes are being written)
+        const int last_plane = a.h0 + t_begin + nload - 1;
+        if (tid == 0) {
+            // every thread finished the previous segment (after()'s barrier)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&bar[s], kBoxBytes);
-            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1,
-                        min(a.h0 + t_begin + it - 2 + STAGES, last_plane));
+            for (int s = 0; s < STAGES && s < niter; ++s) {
+                const int sl = (gbase + s) % STAGES;
+                mbar_expect_tx(&bar[sl], kBoxBytes);
+                tma_load_3d(ring + sl * SLOT, &tmap, &bar[sl], c0, c1,
+                            min(a.h0 + t_begin + s, last_plane));
+            }
         }
-    };
-    bool mine = true;
+
+        auto after = [&](int it) {
+            __syncthreads();
+            // Plane t-2 was last read in this step (level-1 neighbours): its
+            // slot takes plane t-2+STAGES.
+            if (tid == 0 && it >= 2 && it - 2 + STAGES < niter) {
+                const int sl = (gbase + it - 2) % STAGES;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bar[sl], kBoxBytes);
+                tma_load_3d(ring + sl * SLOT, &tmap, &bar[sl], c0, c1,
+                            min(a.h0 + t_begin + it - 2 + STAGES, last_plane));
+            }
+        };
+        bool mine = true;
 #pragma unroll
-    for (int cy = 0; cy < VY; ++cy)
+        for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-        for (int cx = 0; cx < VX; ++cx) mine &= cint[cy][cx];
-    const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in this warp
-    // A unit of three steps runs select-free when the planes its levels read
-    // (t-2K .. t-2) are interior, no column of this warp is on the a1/a2
-    // boundary and every plane level K produces is one of this chunk's
-    // outputs (p = i0 + it - 3K in [i0, i1)); the conditions are monotone in
-    // `it`, so checking the unit's first and last step suffices.
-    // Warp-uniform, decided once per unit.
-    auto clear = [&](int it) {
-        const int t = t_begin + it;
-        return t - 2 * K >= 0 && t - 2 < a.n0 && it >= 3 * K && it < 3 * K + (i1 - i0);
-    };
-#define TB3D_STEP(PH, IT, SEL)                                                                \
-    tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0>(a, out, ring, lev, bar, IT, t_begin, i0, i1, lx, x, y, gx, \
-                                       gy, cint, cout, Hs);                                    \
+            for (int cx = 0; cx < VX; ++cx) mine &= cint[cy][cx];
+        const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in this warp
+        // A unit of three steps runs select-free when the planes its levels
+        // read (t-2K .. t-2) are interior, no column of this warp is on the
+        // a1/a2 boundary and every plane level K produces is one of this
+        // segment's outputs (p = i0 + it - 3K in [i0, i1)); the conditions
+        // are monotone in `it`, so checking the unit's first and last step
+        // suffices.  Warp-uniform, decided once per unit.
+        auto clear = [&](int it) {
+            const int t = t_begin + it;
+            return t - 2 * K >= 0 && t - 2 < a.n0 && it >= 3 * K && it < 3 * K + (i1 - i0);
+        };
+#define TB3D_STEP(PH, IT, SEL)                                                                  \
+    tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0>(a, out, ring, lev, bar, gbase, IT, t_begin, i0, i1, \
+                                               lx, x, y, gx, gy, cint, cout, Hs);               \
     after(IT);
-    for (int it = 0; it < niter; it += 3) {
-        if (warp_int && clear(it) && clear(it + 2)) {
-            TB3D_STEP(0, it, false)
-            TB3D_STEP(1, it + 1, false)
-            TB3D_STEP(2, it + 2, false)
-        } else {
-            TB3D_STEP(0, it, true)
-            if (it + 1 < niter) {
-                TB3D_STEP(1, it + 1, true)
-            }
-            if (it + 2 < niter) {
-                TB3D_STEP(2, it + 2, true)
+        for (int it = 0; it < niter; it += 3) {
+            if (warp_int && clear(it) && clear(it + 2)) {
+                TB3D_STEP(0, it, false)
+                TB3D_STEP(1, it + 1, false)
+                TB3D_STEP(2, it + 2, false)
+            } else {
+                TB3D_STEP(0, it, true)
+                if (it + 1 < niter) {
+                    TB3D_STEP(1, it + 1, true)
+                }
+                if (it + 2 < niter) {
+                    TB3D_STEP(2, it + 2, true)
+                }
             }
         }
+        gbase += niter;
     }
 #undef TB3D_STEP
 }
@@ -400,13 +436,24 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     int per_sm = 1, nsm = 148;
     s = occupancy(tb3d_kernel<T, K, EXACT, G, EARLY0>, G::NT, bytes, &per_sm, &nsm);
     if (!s.ok()) return s;
-    // a0 chunks: whole waves of resident CTAs, >= 48 planes (the 2K-plane
-    // wavefront fill is overhead)
+    // persistent: one CTA per resident slot, each streaming an equal share of
+    // the (tile, plane) positions
     a.lo0 = (int)c.range_lo();
     a.hi0 = (int)c.range_hi();
     if (a.hi0 <= a.lo0) return Status::Ok();
     const int64_t span = a.hi0 - a.lo0;
-    a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 2 * K, 48);
+    const long long total = tiles * span;
+    unsigned grid;
+    if (K == 1) {
+        a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 2 * K, 48);
+        a.per_cta = 0;
+        grid = (unsigned)(tiles * ((span + a.chunk - 1) / a.chunk));
+    } else {
+        const long long ctas = std::min<long long>((long long)nsm * per_sm, total);
+        a.chunk = 0;
+        a.per_cta = (total + ctas - 1) / ctas;
+        grid = (unsigned)((total + a.per_cta - 1) / a.per_cta);
+    }
     a.h0 = (int)g.h[0];
     a.h1 = (int)g.h[1];
     a.off2 = (int)g.off2;
@@ -416,8 +463,6 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.mirror = static_cast<T*>(c.mirror);
     a.mshift = c.mirror_shift;
     for (int q = 0; q < 7; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
-    const long long nchunks = (span + a.chunk - 1) / a.chunk;
-    const unsigned grid = (unsigned)(tiles * nchunks);
     tb3d_kernel<T, K, EXACT, G, EARLY0><<<grid, G::NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
