@@ -61,27 +61,24 @@ struct Vec<double, 4> {
     using type = double4;
 };
 
-template <typename T, int V>
-__device__ __forceinline__ void load_row(const T* __restrict__ p, bool ok, T (&v)[V]) {
-    if (ok) {
-        if constexpr (sizeof(T) * V == 16) {
-            const auto x = __ldg(reinterpret_cast<const typename Vec<T, V>::type*>(p));
-            const T* xs = reinterpret_cast<const T*>(&x);
-#pragma unroll
-            for (int i = 0; i < V; ++i) v[i] = xs[i];
-        } else {
-#pragma unroll
-            for (int i = 0; i < V; i += 16 / (int)sizeof(T)) {
-                const uint4 x = __ldg(reinterpret_cast<const uint4*>(p + i));
-                const T* xs = reinterpret_cast<const T*>(&x);
-#pragma unroll
-                for (int q = 0; q < 16 / (int)sizeof(T); ++q) v[i + q] = xs[q];
-            }
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < V; ++i) v[i] = T(0);
-    }
+// Level-0 rows are staged through a per-warp shared-memory ring filled by
+// cp.async (16 B per lane per row, zero-filled outside the allocation), kDepth
+// rows ahead of use, so DRAM latency hides behind kDepth row steps instead of
+// the 2R+1 a register prefetch can afford.
+constexpr int kDepth = 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gmem),
+                 "r"(ok ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 // One lane's V outputs of a row: a vector store when the whole run is in the
@@ -146,21 +143,35 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     for (int v = 0; v < V; ++v) all_out &= cout[v];
 
     T win[K][P][W];  // ring of rows per level (level K is stored, not kept)
-    T pf[P][V];      // prefetch ring of level-0 rows
+    // staging ring of level-0 rows: kDepth + 1 slots, row t in slot
+    // (t - t_start) % (kDepth + 1); a slot is refilled one step after it was
+    // read, so a lane never overwrites data it has not consumed
+    __shared__ __align__(16) uint4 stage[kWarpsPerBlock][kDepth + 1][32];
+    uint4* my_stage = &stage[threadIdx.x >> 5][0][lane];
 
     const int64_t t_start = rb - (int64_t)K * R;
     const int64_t t_end = re + (int64_t)K * R;  // exclusive
     const T* base_in = in + a.origin + c0;
     T* base_out = out + a.origin + c0;
 
-    auto row_ok = [&](int64_t r) { return r >= -a.hrow && r < a.rows + a.hrow && col_alloc; };
-
-    // Prime the prefetch ring with rows t_start .. t_start+P-1.
-#pragma unroll
-    for (int s = 0; s < P; ++s) {
-        const int64_t r = t_start + s;
-        load_row<T, V>(base_in + r * a.pitch, row_ok(r), pf[s]);
-    }
+    // Fetchable level-0 rows: allocated ([-hrow, rows+hrow)) and inside the
+    // cone (< t_end), for lanes whose columns are allocated; one unsigned
+    // compare per fetch.  Rows advance by one per step: incremental pointer
+    // and ring slots.
+    const int64_t ok_lo = -a.hrow;
+    const uint64_t ok_span = col_alloc ? (uint64_t)(min(a.rows + a.hrow, t_end) - ok_lo) : 0;
+    int64_t fr = t_start;  // next row to fetch
+    const T* fsrc = base_in + t_start * a.pitch;
+    int rd = 0, wr = 0;    // staging slots to read / fill next
+    auto fetch = [&]() {
+        const bool ok = (uint64_t)(fr - ok_lo) < ok_span;
+        cp_async16(my_stage + wr * 32, ok ? (const void*)fsrc : (const void*)in, ok);
+        cp_async_commit();
+        wr = wr == kDepth ? 0 : wr + 1;
+        ++fr;
+        fsrc += a.pitch;
+    };
+    for (int s = 0; s < kDepth; ++s) fetch();
 
     bool mine = true;
 #pragma unroll
@@ -173,11 +184,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     auto step = [&](auto PHc, auto SELc, int64_t t) {
         constexpr int ph = decltype(PHc)::value;
         constexpr bool SEL = decltype(SELc)::value;
-#pragma unroll
-        for (int v = 0; v < V; ++v) win[0][ph][R + v] = pf[ph][v];
         {
-            const int64_t r = t + P;
-            load_row<T, V>(base_in + r * a.pitch, row_ok(r) && r < t_end, pf[ph]);
+            cp_async_wait<kDepth - 1>();  // row t (the oldest pending group) has landed
+            const uint4 raw = my_stage[rd * 32];
+            rd = rd == kDepth ? 0 : rd + 1;
+            const T* rv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+            for (int v = 0; v < V; ++v) win[0][ph][R + v] = rv[v];
+            fetch();  // row t + kDepth, into the slot row t-1 vacated
         }
         if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
 #pragma unroll
