@@ -348,3 +348,31 @@ def test_peer_flags_order_a_stream(ts):
     assert int(flag.item()) == 8
     h, off = _abi.ipc_export(flag.data_ptr())
     assert len(h) == 64 and off >= 0
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
+def test_reduced_shape_full_steps(ts, orc, cfg):
+    """SURVEY §8(d) parity runs: each BASELINE config's kernel, fused depth
+    and dtype on a reduced shape for its FULL step count — exact mode bitwise
+    against the oracle; C4's fast mode (its bench mode) within 1e-5 max-rel
+    and L2-rel as well."""
+    name, ext, dt, steps, fused = {
+        "c2": ("Box-2D9P", [300, 260], "f64", 100, 4),
+        "c3": ("Heat-3D", [40, 44, 48], "f64", 1000, 3),
+        "c4": ("Box-3D27P", [36, 40, 44], "f32", 100, 1),
+        "c5": ("Heat-3D", [64, 36, 40], "f64", 100, 3),
+    }[cfg]
+    k = ts.find_benchmark(name).kernel
+    a = random_grid(ts, orc, ext, [1] * len(ext), 1, dt)
+    ref = a.copy()
+    orc.naive_run(ref, k, steps)
+    got = a.copy()
+    st = ts.run_gpu(got, k, steps, fused_steps=fused, mode="exact")
+    assert st.fused_steps == fused
+    assert both_buffers_equal(got, ref)
+    if cfg == "c4":
+        fast = a.copy()
+        ts.run_gpu(fast, k, steps, fused_steps=fused, mode="fast")
+        d = ts.deviation(fast, ref)
+        assert d["max_rel_deviation"] <= TOL["f32"] and d["l2_rel_err"] <= TOL["f32"]
