@@ -1,4 +1,5 @@
-// stream2d.cu — 2-D star / box sweeps with K time steps fused per HBM pass.
+// stream2d.cu — 2-D star (r = 1, 2) and box (r = 1, 2) sweeps with K time
+// steps fused per HBM pass.
 //
 // Register-level tetrominoes (north_star tier 1) + temporal blocking (tier 2):
 // every warp owns a strip of 32*V columns and streams down the rows.  Each
@@ -264,20 +265,22 @@ bool classify(const TapSet& t, Shape* s) {
         *s = {t.radius, false};
         return true;
     }
-    if (t.shape == TSR_BOX && t.radius == 1) {
-        *s = {1, true};
+    if (t.shape == TSR_BOX && (t.radius == 1 || t.radius == 2)) {
+        *s = {t.radius, true};
         return true;
     }
     return false;
 }
 
 constexpr int kMaxK = 8;
+constexpr int kMaxKBox2 = 2;  // 25-point box: five 6-wide rows per level in registers (k=3 spills)
 
 bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
     Shape s;
     if (!classify(t, &s)) return false;
-    *max_fused = kMaxK;
-    *default_fused = 4;
+    const bool box2 = s.box && s.R == 2;
+    *max_fused = box2 ? kMaxKBox2 : kMaxK;
+    *default_fused = box2 ? 2 : 4;
     return true;
 }
 
@@ -306,7 +309,12 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.row_hi = c.range_hi();
     if (a.row_hi <= a.row_lo) return Status::Ok();
     const int64_t span = a.row_hi - a.row_lo;
-    a.chunk = std::max<int64_t>(16 * K * R, (span + nchunks - 1) / nchunks);
+    // chunks of >= 16*K*R rows keep the 2*K*R-row wavefront fill small; a
+    // grid too small to give every SM a few warps that way (latency-bound)
+    // goes down to 2*K*R-row chunks
+    int64_t min_chunk = 16 * K * R;
+    if (a.nstrips * ((span + min_chunk - 1) / min_chunk) < 148 * 8) min_chunk = 2 * K * R;
+    a.chunk = std::max<int64_t>(min_chunk, (span + nchunks - 1) / nchunks);
     nchunks = (span + a.chunk - 1) / a.chunk;
     a.total_warps = nchunks * a.nstrips;
     for (int t = 0; t < c.taps->ntaps; ++t) a.w[t] = static_cast<T>(c.taps->w[t]);
@@ -342,6 +350,14 @@ template <typename T>
 Status launch_t(const LaunchCtx& c, const void* in, void* out, int k) {
     Shape s;
     classify(*c.taps, &s);
+    if (s.box && s.R == 2) {
+        constexpr int V = 16 / sizeof(T);
+        switch (k) {
+            case 1: return launch_k<T, 2, true, 1, V>(c, in, out);
+            case 2: return launch_k<T, 2, true, 2, V>(c, in, out);
+            default: return Status::Err(TSR_EUNSUPPORTED, "stream2d: 25-point box fuses 1..2");
+        }
+    }
     if (s.box) return launch_shape<T, 1, true>(c, in, out, k);
     if (s.R == 1) return launch_shape<T, 1, false>(c, in, out, k);
     return launch_shape<T, 2, false>(c, in, out, k);

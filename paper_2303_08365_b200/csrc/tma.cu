@@ -17,6 +17,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 int pick_chunk(int64_t n0, int64_t tiles, int64_t slots, int overlap, int min_chunk) {
+    // Grids that cannot fill the GPU with min_chunk-plane chunks (a few
+    // tiles of a small grid) split down to single planes: latency, not the
+    // per-chunk overlap, bounds them.
+    if (tiles * ((n0 + min_chunk - 1) / min_chunk) < slots) min_chunk = 1;
     int64_t best_chunk = n0;
     double best = 1e300;
     for (int64_t nz = 1; nz <= 256; ++nz) {

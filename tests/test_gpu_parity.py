@@ -46,14 +46,16 @@ def test_golden_star2d9p_ttrs(ts, orc):
     assert bitwise_equal_interior(g, golden)
 
 
-@pytest.mark.parametrize("name", ["Heat-2D", "Box-2D9P", "Star-2D9P"])
+@pytest.mark.parametrize("name", ["Heat-2D", "Box-2D9P", "Star-2D9P", "Box-2D25P"])
 @pytest.mark.parametrize("dt", ["f64", "f32"])
 def test_fused_2d_bitwise_all_k(ts, orc, name, dt):
-    """Every fused step count 1..8, T not a multiple of k, ragged extents
-    (narrower than one strip, wider than several), halo wider than r."""
+    """Every fused step count the engine accepts (1..8; 1..2 for the 25-point
+    box), T not a multiple of k, ragged extents (narrower than one strip,
+    wider than several), halo wider than r."""
     k = ts.find_benchmark(name).kernel
     rng = np.random.default_rng(7)
-    for fused in range(1, 9):
+    kmax = 2 if name == "Box-2D25P" else 8
+    for fused in range(1, kmax + 1):
         for extent in ([int(rng.integers(5, 40)), int(rng.integers(5, 30))],
                        [int(rng.integers(60, 130)), int(rng.integers(100, 300))]):
             halo = [k.radius + int(rng.integers(0, 2)), k.radius + int(rng.integers(0, 3))]
