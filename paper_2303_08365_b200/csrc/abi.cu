@@ -21,6 +21,7 @@ extern const Engine kStar3dR1Engine;
 extern const Engine kStream2dEngine;
 extern const Engine kTb3dEngine;
 extern const Engine kBox3dEngine;
+extern const Engine kStream1dEngine;
 
 namespace {
 
@@ -157,7 +158,7 @@ Status check_layout(const Geo& g, const tsr_layout* l) {
 // one by name for A/B measurements; it never falls back to the CPU.
 const Engine* find_engine(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
     static const Engine* const engines[] = {&kTb3dEngine, &kBox3dEngine, &kStar3dR1Engine,
-                                            &kStream2dEngine};
+                                            &kStream2dEngine, &kStream1dEngine};
     const char* pin = std::getenv("TSR_ENGINE");
     for (const Engine* e : engines) {
         if (pin && *pin && std::strcmp(pin, e->name) != 0) continue;

@@ -70,6 +70,28 @@ def test_fused_2d_bitwise_all_k(ts, orc, name, dt):
             assert halos_equal(a, b)
 
 
+@pytest.mark.parametrize("name", ["Heat-1D", "Star-1D5P"])
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_fused_1d_bitwise(ts, orc, name, dt):
+    """The 1-D shared-memory engine: fused depths up to 16, segments shorter
+    and longer than one CTA's 2048 points, halo wider than r, T not a multiple
+    of k — bitwise naive_run, halo untouched."""
+    k = ts.find_benchmark(name).kernel
+    rng = np.random.default_rng(11)
+    for fused in (1, 2, 3, 5, 8, 13, 16):
+        for n in (int(rng.integers(5, 60)), 2048, int(rng.integers(2049, 9000))):
+            halo = [k.radius + int(rng.integers(0, 3))]
+            n = max(n, 2 * halo[0] + 1)
+            steps = int(rng.integers(fused, 3 * fused + 2))
+            a = random_grid(ts, orc, [n], halo, fused * 7 + n, dt)
+            b = a.copy()
+            st = ts.run_gpu(a, k, steps, fused_steps=fused, engine="tuned")
+            orc.naive_run(b, k, steps)
+            assert st.fused_steps == fused and st.engine == "tuned"
+            assert both_buffers_equal(a, b), (fused, n, halo, steps)
+            assert halos_equal(a, b)
+
+
 @pytest.mark.parametrize("fused", [1, 2, 3])
 @pytest.mark.parametrize("dt", ["f64", "f32"])
 def test_heat3d_tuned_bitwise(ts, orc, dt, fused):
@@ -265,7 +287,7 @@ def test_full_shape_properties(ts, orc, cfg):
     ("Box-3D27P", [60, 30, 50], 2, "f64"),   # box3d two-level
     ("Box-2D9P", [200, 150], 4, "f64"),     # stream2d: the range is along the rows
     ("Heat-2D", [120, 90], 6, "f32"),
-    ("Heat-1D", [500], 1, "f64"),           # generic
+    ("Heat-1D", [5000], 8, "f64"),          # stream1d
 ])
 def test_sweep_range_stores_only_its_planes(ts, orc, name, extent, fused, dt):
     """tsr_sweep_range: planes [lo, hi) of axis 0 hold the k-step result
@@ -299,7 +321,7 @@ def test_sweep_range_stores_only_its_planes(ts, orc, name, extent, fused, dt):
     ("Box-3D27P", [30, 30, 50], 1, "f32"),   # box3d
     ("Box-3D27P", [30, 30, 50], 2, "f64"),   # box3d two-level
     ("Box-2D9P", [120, 150], 4, "f64"),     # stream2d
-    ("Heat-1D", [300], 1, "f64"),           # generic
+    ("Heat-1D", [300], 4, "f64"),           # stream1d
 ])
 def test_sweep_range_mirror(ts, orc, name, extent, fused, dt):
     """tsr_sweep_range_mirror (the fused halo exchange): the stored planes

@@ -132,7 +132,7 @@ def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, mode):
     (3, "Box-2D9P", [90, 130], 9, 4),    # stream2d engine
     (2, "Box-3D27P", [40, 30, 50], 4, 1),  # box3d engine
     (2, "Box-3D27P", [44, 30, 50], 5, 2),  # box3d two-level engine
-    (3, "Heat-1D", [300], 6, 1),          # generic engine, 1-D slabs
+    (3, "Heat-1D", [300], 7, 3),          # stream1d engine, 1-D slabs
 ])
 def test_slabs_on_device_equal_oracle(ts, orc, tmp_path, world, name, extent, steps, k, mode):
     """The device slab state (pitched HBM buffers, tsr_advance or
