@@ -47,9 +47,9 @@ CONFIGS = {
                workload="C3: 3D heat 7-point star fp64, 512^3 per GPU, 1000 timesteps",
                ref_tile=[20, 20, 20], ref_tb=10),
     "c4": dict(bench="Box-3D27P", extent=[1024, 1024, 1024], dtype="f32", steps=100, fused=0,
-               mode="fast", strong=True,
+               mode="exact", strong=True,
                workload="C4: 3D 27-point box fp32, 1024^3 global, slab-partitioned over N GPUs "
-                        "(strong scaling), fast (FMA) mode",
+                        "(strong scaling), exact mode (shared 1/27 products: bitwise)",
                ref_tile=None, ref_tb=None),
     "c5": dict(bench="Heat-3D", extent=[1024, 1024, 1024], dtype="f64", steps=100, fused=0,
                mode="exact", workload="C5: 3D heat 7-point fp64, 1024^3 per GPU (weak scaling)",

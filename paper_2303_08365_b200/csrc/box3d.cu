@@ -86,7 +86,9 @@ struct VecT<double, 2> {
 
 // Nine taps of one plane offset applied to the neighbourhood nb (rows y-1..y+VY,
 // cols x-1..x+VX) for every output of the thread's 4x4 tile.
-template <bool EXACT, bool START, typename T>
+// Q: nb holds q = w*v (uniform-weight kernel, see stream2d.cu): every tap is
+// an add of the shared rounded product, bitwise the EXACT sum.
+template <bool EXACT, bool START, typename T, bool Q = false>
 __device__ __forceinline__ void apply9(const T* __restrict__ w, const T (&nb)[VY + 2][VX + 2],
                                        T (&acc)[VY][VX]) {
 #pragma unroll
@@ -100,18 +102,20 @@ __device__ __forceinline__ void apply9(const T* __restrict__ w, const T (&nb)[VY
                 for (int dk = 0; dk < 3; ++dk) {
                     const T v = nb[cy + dj][cx + dk];
                     if (START && dj == 0 && dk == 0)
-                        s = first<EXACT>(w[0], v);
+                        s = Q ? add_rn(T(0), v) : first<EXACT>(w[0], v);
                     else
-                        s = madd<EXACT>(s, w[dj * 3 + dk], v);
+                        s = Q ? add_rn(s, v) : madd<EXACT>(s, w[dj * 3 + dk], v);
                 }
             acc[cy][cx] = s;
         }
 }
 
-template <typename T, bool EXACT>
+// MODE: 0 FAST, 1 EXACT, 2 Q (uniform weights: shared products, exact)
+template <typename T, int MODE>
 __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
                                                    const __grid_constant__ CUtensorMap tmap,
                                                    const __grid_constant__ BoxArgs<T> a) {
+    constexpr bool EXACT = MODE != 0, Q = MODE == 2;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int SLOT = slot1_bytes<T>() / (int)sizeof(T);
     constexpr int BX = BXW1<T>, PL = PAD<T>;
@@ -180,6 +184,12 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
             }
             nb[r][VX + 1] = row[VX];
         }
+        if constexpr (Q) {
+#pragma unroll
+            for (int r = 0; r < VY + 2; ++r)
+#pragma unroll
+                for (int c = 0; c < VX + 2; ++c) nb[r][c] = mul_rn(a.w[0], nb[r][c]);
+        }
         __syncthreads();  // every thread has its neighbourhood: slot may be refilled
         if (tid == 0 && it + STAGES < niter) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -188,7 +198,7 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
                         a.h0 + t_begin + it + STAGES);
         }
         // finish output q-1 (di = +1 taps)
-        apply9<EXACT, false>(a.w + 18, nb, accB);
+        apply9<EXACT, false, T, Q>(a.w + 18, nb, accB);
         const int po = q - 1;
         if (it >= 2 && po < i1) {
             T* o = out + a.origin + (long long)po * a.pitch0 + (long long)(gy + y) * a.pitch1 +
@@ -201,12 +211,12 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
             }
         }
         // output q continues (di = 0), output q+1 starts (di = -1)
-        apply9<EXACT, false>(a.w + 9, nb, accA);
+        apply9<EXACT, false, T, Q>(a.w + 9, nb, accA);
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < VX; ++cx) accB[cy][cx] = accA[cy][cx];
-        apply9<EXACT, true>(a.w, nb, accA);
+        apply9<EXACT, true, T, Q>(a.w, nb, accA);
     }
 }
 
@@ -240,10 +250,11 @@ constexpr int smem2_bytes() {
     return STAGES * slot_bytes<T>() + NB * b_bytes<T>() + STAGES * 8;
 }
 
-template <typename T, bool EXACT>
+template <typename T, int MODE>
 __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
                                                       const __grid_constant__ CUtensorMap tmap,
                                                       const __grid_constant__ BoxArgs<T> a) {
+    constexpr bool EXACT = MODE != 0, Q = MODE == 2;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
     constexpr int BE = b_bytes<T>() / (int)sizeof(T);
@@ -332,24 +343,30 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
         const bool sel = !(warp_int && q - 2 >= 0 && q < a.n0);  // planes q-2..q
         T nb[VY + 2][VX + 2];
         read_nb(ring + slot * SLOT + PL + x, BX, nb);
+        if constexpr (Q) {  // level 0 -> q; level-1 planes are published as q
+#pragma unroll
+            for (int r = 0; r < VY + 2; ++r)
+#pragma unroll
+                for (int c = 0; c < VX + 2; ++c) nb[r][c] = mul_rn(a.w[0], nb[r][c]);
+        }
         // level 1: finish q-1, continue q, start q+1
-        apply9<EXACT, false>(a.w + 18, nb, a1B);
+        apply9<EXACT, false, T, Q>(a.w + 18, nb, a1B);
         T l1[VY][VX];
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < VX; ++cx) {
-                l1[cy][cx] = a1B[cy][cx];
+                l1[cy][cx] = Q ? mul_rn(a.w[0], a1B[cy][cx]) : a1B[cy][cx];
                 if (sel && !(cint[cy][cx] && q - 1 >= 0 && q - 1 < a.n0))
                     l1[cy][cx] = keep0[cy][cx];
                 keep0[cy][cx] = nb[cy + 1][cx + 1];
             }
-        apply9<EXACT, false>(a.w + 9, nb, a1A);
+        apply9<EXACT, false, T, Q>(a.w + 9, nb, a1A);
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < VX; ++cx) a1B[cy][cx] = a1A[cy][cx];
-        apply9<EXACT, true>(a.w, nb, a1A);
+        apply9<EXACT, true, T, Q>(a.w, nb, a1A);
         // publish level-1 plane q-1: cell (y, x) at row y+1, column x+PAD
         T* B = buf + (((q - 1) % NB + NB) % NB) * BE;
 #pragma unroll
@@ -373,7 +390,7 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
         // level 2 on level-1 plane q-1: finish q-2, continue q-1, start q
         T nb2[VY + 2][VX + 2];
         read_nb(B + PL + x, BW, nb2);  // buffer rows y..y+VY+1 = region rows y-1..y+VY
-        apply9<EXACT, false>(a.w + 18, nb2, a2B);
+        apply9<EXACT, false, T, Q>(a.w + 18, nb2, a2B);
         const int po = q - 2;
         if (it >= 4 && po < i1) {
             // stored cells are interior (cout implies cint): no Dirichlet select
@@ -388,12 +405,12 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
                 if (a.mirror) store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, v, cout[cy]);
             }
         }
-        apply9<EXACT, false>(a.w + 9, nb2, a2A);
+        apply9<EXACT, false, T, Q>(a.w + 9, nb2, a2A);
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < VX; ++cx) a2B[cy][cx] = a2A[cy][cx];
-        apply9<EXACT, true>(a.w, nb2, a2A);
+        apply9<EXACT, true, T, Q>(a.w, nb2, a2A);
     }
 }
 
@@ -405,7 +422,7 @@ bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused)
     return true;
 }
 
-template <typename T, bool EXACT>
+template <typename T, int MODE>
 Status launch(const LaunchCtx& c, const void* in, void* out) {
     const Geo& g = *c.g;
     CUtensorMap map;
@@ -428,7 +445,7 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     for (int q = 0; q < 27; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     constexpr int bytes = smem_bytes<T>();
     int per_sm = 1, nsm = 148;
-    s = occupancy(box3d_kernel<T, EXACT>, NT1<T>, bytes, &per_sm, &nsm);
+    s = occupancy(box3d_kernel<T, MODE>, NT1<T>, bytes, &per_sm, &nsm);
     if (!s.ok()) return s;
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
     a.lo0 = (int)c.range_lo();
@@ -437,13 +454,13 @@ Status launch(const LaunchCtx& c, const void* in, void* out) {
     const int64_t span = a.hi0 - a.lo0;
     a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 2, 32);
     const long long nchunks = (span + a.chunk - 1) / a.chunk;
-    box3d_kernel<T, EXACT><<<(unsigned)(tiles * nchunks), NT1<T>, bytes, c.stream>>>(
+    box3d_kernel<T, MODE><<<(unsigned)(tiles * nchunks), NT1<T>, bytes, c.stream>>>(
         static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
 }
 
-template <typename T, bool EXACT>
+template <typename T, int MODE>
 Status launch2(const LaunchCtx& c, const void* in, void* out) {
     const Geo& g = *c.g;
     CUtensorMap map;
@@ -466,7 +483,7 @@ Status launch2(const LaunchCtx& c, const void* in, void* out) {
     for (int q = 0; q < 27; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     constexpr int bytes = smem2_bytes<T>();
     int per_sm = 1, nsm = 148;
-    s = occupancy(box3d_tb2_kernel<T, EXACT>, NT, bytes, &per_sm, &nsm);
+    s = occupancy(box3d_tb2_kernel<T, MODE>, NT, bytes, &per_sm, &nsm);
     if (!s.ok()) return s;
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
     a.lo0 = (int)c.range_lo();
@@ -475,22 +492,27 @@ Status launch2(const LaunchCtx& c, const void* in, void* out) {
     const int64_t span = a.hi0 - a.lo0;
     a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 4, 32);
     const long long nchunks = (span + a.chunk - 1) / a.chunk;
-    box3d_tb2_kernel<T, EXACT><<<(unsigned)(tiles * nchunks), NT, bytes, c.stream>>>(
+    box3d_tb2_kernel<T, MODE><<<(unsigned)(tiles * nchunks), NT, bytes, c.stream>>>(
         static_cast<T*>(out), map, a);
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
 }
 
-Status run(const LaunchCtx& c, const void* in, void* out, int k) {
+template <typename T>
+Status run_t(const LaunchCtx& c, const void* in, void* out, int k) {
+    const int mode = uniform_weights(*c.taps) ? 2 : c.exact ? 1 : 0;  // Q serves both modes
     if (k == 2) {
-        if (c.g->dtype == TSR_F64)
-            return c.exact ? launch2<double, true>(c, in, out) : launch2<double, false>(c, in, out);
-        return c.exact ? launch2<float, true>(c, in, out) : launch2<float, false>(c, in, out);
+        if (mode == 2) return launch2<T, 2>(c, in, out);
+        return mode ? launch2<T, 1>(c, in, out) : launch2<T, 0>(c, in, out);
     }
     if (k != 1) return Status::Err(TSR_EUNSUPPORTED, "box3d fuses one or two steps per pass");
-    if (c.g->dtype == TSR_F64)
-        return c.exact ? launch<double, true>(c, in, out) : launch<double, false>(c, in, out);
-    return c.exact ? launch<float, true>(c, in, out) : launch<float, false>(c, in, out);
+    if (mode == 2) return launch<T, 2>(c, in, out);
+    return mode ? launch<T, 1>(c, in, out) : launch<T, 0>(c, in, out);
+}
+
+Status run(const LaunchCtx& c, const void* in, void* out, int k) {
+    if (c.g->dtype == TSR_F64) return run_t<double>(c, in, out, k);
+    return run_t<float>(c, in, out, k);
 }
 
 }  // namespace

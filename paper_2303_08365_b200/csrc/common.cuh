@@ -150,6 +150,20 @@ __device__ __forceinline__ void store_row(T* o, const T (&v)[N], const bool (&ok
     }
 }
 
+// Correctly rounded multiply / add, never contracted into an FMA.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+// True when every tap carries the same weight (the reference's box kernels:
+// 1/9, 1/25, 1/27): engines then share one rounded product per input value.
+inline bool uniform_weights(const TapSet& t) {
+    for (int i = 1; i < t.ntaps; ++i)
+        if (t.w[i] != t.w[0]) return false;
+    return true;
+}
+
 // Compile-time loop: f(std::integral_constant<int, i>) for i in [0, N).
 template <int I, int N, typename F>
 __device__ __forceinline__ void static_for(F&& f) {

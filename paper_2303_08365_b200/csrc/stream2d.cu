@@ -115,9 +115,17 @@ __device__ __forceinline__ void exchange(T (&row)[V + 2 * R]) {
     }
 }
 
-template <typename T, int R, bool BOX, int K, int V, bool EXACT>
+// MODE: 0 = FAST (FMA per tap), 1 = EXACT (multiply, then add, per tap),
+// 2 = Q (exact, for kernels whose taps all carry one weight w, e.g. the
+// reference's Box-2D9P / Box-2D25P): the level windows hold q = w*v, the
+// product every tap of every output reading v computes — rounded once, shared
+// by all of them, so each update is a chain of adds and the next level's q is
+// one multiply per produced value.  Bitwise equal to EXACT.
+template <typename T, int R, bool BOX, int K, int V, int MODE>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     const T* __restrict__ in, T* __restrict__ out, const __grid_constant__ S2Args<T> a) {
+    constexpr bool EXACT = MODE != 0;
+    constexpr bool QS = MODE == 2;
     constexpr int P = 2 * R + 1;  // ring depth per level
     constexpr int W = V + 2 * R;  // values per ring row incl. lane halo
     const int lane = threadIdx.x & 31;
@@ -191,7 +199,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
             rd = rd == kDepth ? 0 : rd + 1;
             const T* rv = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-            for (int v = 0; v < V; ++v) win[0][ph][R + v] = rv[v];
+            for (int v = 0; v < V; ++v) win[0][ph][R + v] = QS ? mul_rn(a.w[0], rv[v]) : rv[v];
             fetch();  // row t + kDepth, into the slot row t-1 vacated
         }
         if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
@@ -215,17 +223,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
                     for (int dc = -R; dc <= R; ++dc) {
                         if (has_tap<R, BOX>(dr, dc)) {
                             const T xv = win[l - 1][sr][R + v + dc];
-                            acc = tap == 0 ? lead(a.w[0], xv) : madd<EXACT>(acc, a.w[tap], xv);
+                            if constexpr (QS)
+                                acc = tap == 0 ? xv : add_rn(acc, xv);
+                            else
+                                acc = tap == 0 ? lead(a.w[0], xv) : madd<EXACT>(acc, a.w[tap], xv);
                             ++tap;
                         }
                     }
                 }
+                // level K only stores interior cells: no Dirichlet select
+                T nv = acc;
+                if (l < K && QS) nv = mul_rn(a.w[0], acc);  // the next level's q
                 if constexpr (SEL) {
                     const bool rint = x >= 0 && x < a.rows;
-                    res[v] = (rint && cint[v]) ? acc : win[l - 1][sx][R + v];
-                } else {
-                    res[v] = acc;
+                    if (l < K) nv = (rint && cint[v]) ? nv : win[l - 1][sx][R + v];
                 }
+                res[v] = nv;
             }
             if (l < K) {
 #pragma unroll
@@ -320,11 +333,19 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     for (int t = 0; t < c.taps->ntaps; ++t) a.w[t] = static_cast<T>(c.taps->w[t]);
     const unsigned blocks =
         static_cast<unsigned>((a.total_warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    if constexpr (BOX) {
+        if (uniform_weights(*c.taps)) {  // Q mode serves exact and fast alike
+            stream2d_kernel<T, R, BOX, K, V, 2><<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
+                static_cast<const T*>(in), static_cast<T*>(out), a);
+            TSR_CUDA_TRY(cudaGetLastError());
+            return Status::Ok();
+        }
+    }
     if (c.exact)
-        stream2d_kernel<T, R, BOX, K, V, true><<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
+        stream2d_kernel<T, R, BOX, K, V, 1><<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
             static_cast<const T*>(in), static_cast<T*>(out), a);
     else
-        stream2d_kernel<T, R, BOX, K, V, false><<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
+        stream2d_kernel<T, R, BOX, K, V, 0><<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
             static_cast<const T*>(in), static_cast<T*>(out), a);
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
