@@ -96,6 +96,19 @@ def plan_slabs(global_extent, radius: int, fused_steps: int, world: int, rank: i
                     own_hi, ghost_lo, ghost_hi, depth * cross * esize)
 
 
+def mirror_shift(plan: SlabPlan, side: str) -> int:
+    """Plane shift of a seam pass on `side` ("lo" or "hi"): my boundary own
+    plane at local row j lands on the neighbour's ghost plane at local row
+    j + shift (its ghost_hi planes for "lo", its ghost_lo planes for "hi")."""
+    if side == "lo":
+        nb = plan_slabs(plan.global_extent, plan.radius, plan.fused_steps, plan.world,
+                        plan.rank - 1, plan.halo)
+        return (nb.ghost_lo + nb.own) - plan.ghost_lo
+    if side == "hi":
+        return -(plan.ghost_lo + plan.own - plan.depth)
+    raise ValueError("side must be 'lo' or 'hi'")
+
+
 def local_from_global(global_grid, plan: SlabPlan, poison: bool = False):
     """Host local slab: owned rows + ghost rows (+ global halo at the true
     ends) copied from a global host grid (HaloWorker::copy_from_global,
@@ -273,14 +286,8 @@ class PeerLink:
                 if not 0 <= nb < plan.world:
                     continue
                 peer = info[nb]
-                nplan = plan_slabs(plan.global_extent, plan.radius, plan.fused_steps, plan.world,
-                                   nb, plan.halo)
-                if side == "lo":  # my first own planes -> its ghost_hi planes
-                    shift = (nplan.ghost_lo + nplan.own) - plan.ghost_lo
-                    word = 1
-                else:             # my last own planes -> its ghost_lo planes (rows 0..d)
-                    shift = -(plan.ghost_lo + plan.own - plan.depth)
-                    word = 0
+                shift = mirror_shift(plan, side)
+                word = 1 if side == "lo" else 0  # the flag word of mine it counts in
                 self.peer[side] = {"buf": [self._map(*peer["buf"][0]),
                                            self._map(*peer["buf"][1])],
                                    "flag": self._map(*peer["flags"]) + 4 * word,

@@ -153,3 +153,32 @@ def test_slabs_on_device_equal_oracle(ts, orc, tmp_path, world, name, extent, st
     want = ref.padded(ref.parity)[h:h + extent[0]]
     assert np.isfinite(got).all()
     assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("world,n0,radius,k", [(2, 128, 1, 3), (3, 61, 1, 2), (4, 40, 2, 2),
+                                               (8, 1024, 1, 3), (5, 23, 1, 4)])
+def test_peer_mirror_shift_lands_on_neighbour_ghosts(world, n0, radius, k):
+    """The plane shift PeerLink gives each seam pass maps the sender's
+    boundary own planes exactly onto the receiver's ghost planes, in the
+    receiver's local coordinates (so a round's seam passes deliver the same
+    planes the NCCL transport sends)."""
+    from paper_2303_08365_b200.partition import mirror_shift, plan_slabs
+    plans = [plan_slabs([n0, 7], radius, k, world, r) for r in range(world)]
+    for r, p in enumerate(plans):
+        g = lambda plan, local: local - plan.ghost_lo + plan.own_lo  # local row -> global row
+        if r > 0:  # lo seam: my first depth own planes -> lo neighbour's ghost_hi planes
+            nb = plans[r - 1]
+            shift = mirror_shift(p, "lo")
+            for j in range(p.depth):
+                mine = p.ghost_lo + j
+                theirs = mine + shift
+                assert nb.ghost_lo + nb.own <= theirs < nb.local_extent[0]
+                assert g(p, mine) == g(nb, theirs)
+        if r < world - 1:  # hi seam: my last depth own planes -> hi neighbour's ghost_lo
+            nb = plans[r + 1]
+            shift = mirror_shift(p, "hi")
+            for j in range(p.depth):
+                mine = p.ghost_lo + p.own - p.depth + j
+                theirs = mine + shift
+                assert 0 <= theirs < nb.ghost_lo
+                assert g(p, mine) == g(nb, theirs)
