@@ -144,7 +144,7 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 // (q - t_begin) % 3 == s, so the window rotates by renaming (loop unrolled
 // by 3).  a1-neighbour rows of other warps are read two steps after they
 // were written (3-deep SMEM buffers, one __syncthreads per step).
-template <typename T, int K, bool EXACT, int PH, bool SEL, typename G, bool EARLY0>
+template <typename T, int K, bool EXACT, int PH, bool SEL, typename G, bool EARLY0, bool MIRROR>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
                                           uint64_t* bar, unsigned gbase, int it, int t_begin,
                                           int i0, int i1, int lx, int x, int y, int gx, int gy,
@@ -193,8 +193,12 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
             T left = __shfl_up_sync(0xffffffffu, c1v, 1);
             T right = __shfl_down_sync(0xffffffffu, c0v, 1);
             if (l == 1) {  // region-1 edge columns read the level-0 halo ring
-                if (lx == 0) left = Pm[(y + cy + 1) * BX + PL - 1];
-                if (lx == NLX - 1) right = Pm[(y + cy + 1) * BX + R1X + PL];
+                // every lane loads the two edge cells (one broadcast wavefront
+                // each) and the edge lanes select them: no divergent branch
+                const T el = Pm[(y + cy + 1) * BX + PL - 1];
+                const T er = Pm[(y + cy + 1) * BX + R1X + PL];
+                left = lx == 0 ? el : left;
+                right = lx == NLX - 1 ? er : right;
             }
             const T up0 = cy == 0 ? u.x : Hs[l - 1][sC][cy - 1][0];
             const T up1 = cy == 0 ? u.y : Hs[l - 1][sC][cy - 1][1];
@@ -237,8 +241,20 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                 T v[VX];
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) v[cx] = fix_zero<EXACT>(res[cy][cx]);
-                store_row<T, VX>(o + cy * a.pitch1, v, cout[cy]);
-                if (a.mirror) store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, v, cout[cy]);
+                if constexpr (!SEL && VX * sizeof(T) == 16) {
+                    // select-free warps have no boundary column: a lane's two
+                    // columns are both in or both out of the output tile
+                    if (cout[cy][0]) {
+                        *reinterpret_cast<P2*>(o + cy * a.pitch1) = P2{v[0], v[1]};
+                        if constexpr (MIRROR)
+                            *reinterpret_cast<P2*>(a.mirror + (o - out) + a.mshift + cy * a.pitch1) =
+                                P2{v[0], v[1]};
+                    }
+                } else {
+                    store_row<T, VX>(o + cy * a.pitch1, v, cout[cy]);
+                    if constexpr (MIRROR)
+                        store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, v, cout[cy]);
+                }
             }
         }
     }
@@ -253,7 +269,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
     }
 }
 
-template <typename T, int K, bool EXACT, typename G, bool EARLY0>
+template <typename T, int K, bool EXACT, typename G, bool EARLY0, bool MIRROR>
 __global__ void __launch_bounds__(G::NT, 1)
     tb3d_kernel(T* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
                 const __grid_constant__ TbArgs<T> a) {
@@ -384,7 +400,7 @@ __global__ void __launch_bounds__(G::NT, 1)
             return t - 2 * K >= 0 && t - 2 < a.n0 && it >= 3 * K && it < 3 * K + (i1 - i0);
         };
 #define TB3D_STEP(PH, IT, SEL)                                                                  \
-    tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0>(a, out, ring, lev, bar, gbase, IT, t_begin, i0, i1, \
+    tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0, MIRROR>(a, out, ring, lev, bar, gbase, IT, t_begin, i0, i1, \
                                                lx, x, y, gx, gy, cint, cout, Hs);               \
     after(IT);
         for (int it = 0; it < niter; it += 3) {
@@ -434,7 +450,7 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     const long long tiles = (long long)a.tiles_x * a.tiles_y;
     constexpr int bytes = smem_bytes<T, K, G>();
     int per_sm = 1, nsm = 148;
-    s = occupancy(tb3d_kernel<T, K, EXACT, G, EARLY0>, G::NT, bytes, &per_sm, &nsm);
+    s = occupancy(tb3d_kernel<T, K, EXACT, G, EARLY0, false>, G::NT, bytes, &per_sm, &nsm);
     if (!s.ok()) return s;
     // persistent: one CTA per resident slot, each streaming an equal share of
     // the (tile, plane) positions
@@ -463,7 +479,15 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.mirror = static_cast<T*>(c.mirror);
     a.mshift = c.mirror_shift;
     for (int q = 0; q < 7; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
-    tb3d_kernel<T, K, EXACT, G, EARLY0><<<grid, G::NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);
+    if (c.mirror) {
+        TSR_CUDA_TRY(cudaFuncSetAttribute(tb3d_kernel<T, K, EXACT, G, EARLY0, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        tb3d_kernel<T, K, EXACT, G, EARLY0, true><<<grid, G::NT, bytes, c.stream>>>(
+            static_cast<T*>(out), map, a);
+    } else {
+        tb3d_kernel<T, K, EXACT, G, EARLY0, false><<<grid, G::NT, bytes, c.stream>>>(
+            static_cast<T*>(out), map, a);
+    }
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
 }
