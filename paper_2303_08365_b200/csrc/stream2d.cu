@@ -158,17 +158,25 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     __shared__ __align__(16) uint4 stage[kWarpsPerBlock][kDepth + 1][32];
     uint4* my_stage = &stage[threadIdx.x >> 5][0][lane];
 
-    const int64_t t_start = rb - (int64_t)K * R;
-    const int64_t t_end = re + (int64_t)K * R;  // exclusive
+    // Level l produces row t - l*S at step t.  S = R (EXACT/FAST): level l
+    // reads the row level l-1 produced in the same step.  S = R+1 (Q mode,
+    // whose updates are pure add chains and latency-bound): every row a
+    // level reads was produced in an earlier step, so the K levels of a step
+    // are independent chains (levels run in descending order, level 0 last).
+    constexpr bool SKEW = QS && R == 1;  // (the 25-point box measured slower skewed)
+    constexpr int S = SKEW ? R + 1 : R;
+    const int64_t t_start = rb - (int64_t)K * R;  // first level-0 row of the cone
+    const int64_t t_end = re + (int64_t)K * S;    // exclusive: level K stores row re-1
+    const int64_t cone_end = re + (int64_t)K * R; // level-0 rows [t_start, cone_end)
     const T* base_in = in + a.origin + c0;
     T* base_out = out + a.origin + c0;
 
     // Fetchable level-0 rows: allocated ([-hrow, rows+hrow)) and inside the
-    // cone (< t_end), for lanes whose columns are allocated; one unsigned
+    // cone (< cone_end), for lanes whose columns are allocated; one unsigned
     // compare per fetch.  Rows advance by one per step: incremental pointer
     // and ring slots.
     const int64_t ok_lo = -a.hrow;
-    const uint64_t ok_span = col_alloc ? (uint64_t)(min(a.rows + a.hrow, t_end) - ok_lo) : 0;
+    const uint64_t ok_span = col_alloc ? (uint64_t)(min(a.rows + a.hrow, cone_end) - ok_lo) : 0;
     int64_t fr = t_start;  // next row to fetch
     const T* fsrc = base_in + t_start * a.pitch;
     int rd = 0, wr = 0;    // staging slots to read / fill next
@@ -187,26 +195,31 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     for (int v = 0; v < V; ++v) mine &= cint[v];
     const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in the strip
 
-    // One row step: level 0 takes row t, level l produces row t - l*R.
+    // Level 0 takes row t from the staging ring into window slot ph.
+    auto level0 = [&](auto PHc) {
+        constexpr int ph = decltype(PHc)::value;
+        cp_async_wait<kDepth - 1>();  // row t (the oldest pending group) has landed
+        const uint4 raw = my_stage[rd * 32];
+        rd = rd == kDepth ? 0 : rd + 1;
+        const T* rv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int v = 0; v < V; ++v) win[0][ph][R + v] = QS ? mul_rn(a.w[0], rv[v]) : rv[v];
+        fetch();  // row t + kDepth, into the slot row t-1 vacated
+        if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
+    };
+
+    // One row step: level 0 takes row t, level l produces row t - l*S.
     // SEL = false is the select-free instantiation for steps where every
     // produced row and every column of the warp is interior.
     auto step = [&](auto PHc, auto SELc, int64_t t) {
         constexpr int ph = decltype(PHc)::value;
         constexpr bool SEL = decltype(SELc)::value;
-        {
-            cp_async_wait<kDepth - 1>();  // row t (the oldest pending group) has landed
-            const uint4 raw = my_stage[rd * 32];
-            rd = rd == kDepth ? 0 : rd + 1;
-            const T* rv = reinterpret_cast<const T*>(&raw);
+        if constexpr (!SKEW) level0(PHc);
 #pragma unroll
-            for (int v = 0; v < V; ++v) win[0][ph][R + v] = QS ? mul_rn(a.w[0], rv[v]) : rv[v];
-            fetch();  // row t + kDepth, into the slot row t-1 vacated
-        }
-        if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
-#pragma unroll
-        for (int l = 1; l <= K; ++l) {
-            const int64_t x = t - (int64_t)l * R;
-            const int sx = ((ph - l * R) % P + P) % P;  // slot of row x (static)
+        for (int li = 0; li < K; ++li) {
+            const int l = SKEW ? K - li : 1 + li;
+            const int64_t x = t - (int64_t)l * S;
+            const int sx = ((ph - l * S) % P + P) % P;  // slot of row x (static)
             // Star taps read lane-halo columns of the centre row only:
             // exchange it at use, so the halos of the other rows never
             // occupy registers.  Box rows carry halos from production.
@@ -252,13 +265,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
                 if (a.mirror) store_vals<T, V>(a.mirror + (dst - out) + a.mshift, res, cout, all_out);
             }
         }
+        if constexpr (SKEW) level0(PHc);  // row t replaces row t-P, which level 1 has just read
     };
 
     for (int64_t tb = t_start; tb < t_end; tb += P) {
         static_for<0, P>([&](auto PHc) {
             const int64_t t = tb + decltype(PHc)::value;
             if (t < t_end) {
-                if (warp_int && t - (int64_t)K * R >= 0 && t - R < a.rows)
+                if (warp_int && t - (int64_t)K * S >= 0 && t - S < a.rows)
                     step(PHc, std::false_type{}, t);
                 else
                     step(PHc, std::true_type{}, t);
