@@ -157,16 +157,23 @@ def cpu_baseline(ts, cfg, cfg_name, steps_cap=None):
     k = ts.find_benchmark(cfg["bench"]).kernel
     if cfg["dtype"] == "f64":
         extent = cfg["extent"]
+        tb = cfg["ref_tb"]
         g = make_grid(ts, cfg, extent)
-        steps = cfg["ref_tb"] * (1 if steps_cap is None else max(1, steps_cap // cfg["ref_tb"]))
-        (upd, rounds, trailing), sec = ref.run_tessellated(g, k, steps, cfg["ref_tile"],
-                                                           cfg["ref_tb"], threads)
+        steps = tb * (1 if steps_cap is None else max(1, steps_cap // tb))
+        (upd, rounds, trailing), sec = ref.run_tessellated(g, k, steps, cfg["ref_tile"], tb,
+                                                           threads)
+        if steps_cap is None and sec < 5.0:
+            # bounded sample of about 10 s of CPU work (whole tb rounds)
+            steps = tb * max(1, min(40, round(10.0 / max(sec, 1e-3))))
+            g = make_grid(ts, cfg, extent)
+            (upd, rounds, trailing), sec = ref.run_tessellated(g, k, steps, cfg["ref_tile"],
+                                                               tb, threads)
         value = upd / sec / 1e9
         return {"value": round(value, 4), "unit": "GStencil/s", "cores": threads,
                 "kind": "reference",
                 "sample": (f"reference run_tessellated(tile={cfg['ref_tile']}, "
-                           f"tb={cfg['ref_tb']}, threads={threads}) on the full "
-                           f"{'x'.join(map(str, extent))} grid, T={steps}")}
+                           f"tb={tb}, threads={threads}) on the full "
+                           f"{'x'.join(map(str, extent))} grid, T={steps} ({sec:.1f} s)")}
     # fp32: the reference has no threaded fp32 path; naive_run<float>, 1 thread,
     # on a slab of the full cross-section.
     extent = [64] + cfg["extent"][1:]
