@@ -290,7 +290,8 @@ def main():
         try:
             runner = SlabRunner.synthetic(ts, k, plan, cfg["dtype"], dev, seed=1 + rank,
                                           fused_steps=fused_req, mode=mode,
-                                          overlap=not args.no_overlap, transport=args.transport)
+                                          overlap=not args.no_overlap, transport=args.transport,
+                                          graphs=args.transport == "peer")
         except Exception as e:  # IPC mapping refused on this box: message transport
             if args.transport != "peer":
                 raise

@@ -181,6 +181,15 @@ int tsr_ipc_close(void* base);
  * `stream` until the word reaches `value` (wrap-around compare). */
 int tsr_peer_signal(void* flag, uint32_t value, void* stream);
 int tsr_peer_wait(const void* flag, uint32_t value, void* stream);
+/* Round-counting forms for graph-captured rounds (no per-round arguments):
+ * `counter` (local) holds the rounds this rank has completed.
+ * tsr_peer_round_wait holds `stream` until each non-NULL local flag word
+ * (rounds completed by the lo / hi neighbour) reaches *counter;
+ * tsr_peer_round_signal increments *counter and stores it, system-scope
+ * release, into each non-NULL peer-mapped flag word. */
+int tsr_peer_round_wait(const void* flag_lo, const void* flag_hi, const void* counter,
+                        void* stream);
+int tsr_peer_round_signal(void* peer_lo, void* peer_hi, void* counter, void* stream);
 
 /* Reports the engine (tsr_engine) and fused step count k tsr_advance /
  * tsr_run would use for this kernel, grid and opts (no device work). */

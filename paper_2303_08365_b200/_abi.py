@@ -27,7 +27,7 @@ EXPORTED = (
     "tsr_fill_random", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
     "tsr_copy_halo", "tsr_advance", "tsr_query_plan", "tsr_apply_box", "tsr_sweep_range",
     "tsr_sweep_range_mirror", "tsr_ipc_export", "tsr_ipc_open", "tsr_ipc_close",
-    "tsr_peer_signal", "tsr_peer_wait",
+    "tsr_peer_signal", "tsr_peer_wait", "tsr_peer_round_wait", "tsr_peer_round_signal",
 )
 
 
@@ -140,6 +140,8 @@ def lib() -> ctypes.CDLL:
         L.tsr_ipc_close.argtypes = [c_void_p]
         L.tsr_peer_signal.argtypes = [c_void_p, ctypes.c_uint32, c_void_p]
         L.tsr_peer_wait.argtypes = [c_void_p, ctypes.c_uint32, c_void_p]
+        L.tsr_peer_round_wait.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
+        L.tsr_peer_round_signal.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
         for name in EXPORTED:
             if name not in ("tsr_abi_version", "tsr_last_error"):
                 getattr(L, name).restype = ctypes.c_int

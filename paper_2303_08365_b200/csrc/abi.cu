@@ -466,6 +466,9 @@ using namespace tsr;
 namespace tsr {
 Status peer_signal(void* flag, unsigned value, cudaStream_t s);
 Status peer_wait(const void* flag, unsigned value, cudaStream_t s);
+Status peer_round_wait(const void* flag_lo, const void* flag_hi, const void* counter,
+                       cudaStream_t s);
+Status peer_round_signal(void* peer_lo, void* peer_hi, void* counter, cudaStream_t s);
 Status ipc_export(const void* ptr, unsigned char* handle, int64_t* offset);
 Status ipc_open(const unsigned char* handle, void** base);
 Status ipc_close(void* base);
@@ -622,6 +625,17 @@ int tsr_peer_signal(void* flag, uint32_t value, void* stream) {
 int tsr_peer_wait(const void* flag, uint32_t value, void* stream) {
     if (!flag) return report(Status::Err(TSR_EINVAL, "null flag"));
     return report(peer_wait(flag, value, static_cast<cudaStream_t>(stream)));
+}
+
+int tsr_peer_round_wait(const void* flag_lo, const void* flag_hi, const void* counter,
+                        void* stream) {
+    if (!counter) return report(Status::Err(TSR_EINVAL, "null counter"));
+    return report(peer_round_wait(flag_lo, flag_hi, counter, static_cast<cudaStream_t>(stream)));
+}
+
+int tsr_peer_round_signal(void* peer_lo, void* peer_hi, void* counter, void* stream) {
+    if (!counter) return report(Status::Err(TSR_EINVAL, "null counter"));
+    return report(peer_round_signal(peer_lo, peer_hi, counter, static_cast<cudaStream_t>(stream)));
 }
 
 int tsr_ipc_export(const void* ptr, tsr_ipc_handle* handle, int64_t* offset) {

@@ -40,6 +40,32 @@ __global__ void wait_kernel(const unsigned* flag, unsigned value) {
     }
 }
 
+// Round-counting variants (no per-round kernel arguments, so a round can be
+// captured once into a CUDA graph and replayed): `counter` holds the rounds
+// this rank has completed.
+__global__ void round_wait_kernel(const unsigned* flag_lo, const unsigned* flag_hi,
+                                  const unsigned* counter) {
+    unsigned want;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(want) : "l"(counter) : "memory");
+    for (const unsigned* f : {flag_lo, flag_hi}) {
+        if (!f) continue;
+        for (;;) {
+            unsigned v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if (static_cast<int>(v - want) >= 0) break;
+            __nanosleep(200);
+        }
+    }
+}
+
+__global__ void round_signal_kernel(unsigned* peer_lo, unsigned* peer_hi, unsigned* counter) {
+    __threadfence_system();
+    const unsigned done = *counter + 1;
+    *counter = done;
+    for (unsigned* f : {peer_lo, peer_hi})
+        if (f) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(done) : "memory");
+}
+
 using GetRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 GetRangeFn get_range() {
@@ -65,6 +91,23 @@ Status peer_signal(void* flag, unsigned value, cudaStream_t s) {
 
 Status peer_wait(const void* flag, unsigned value, cudaStream_t s) {
     wait_kernel<<<1, 1, 0, s>>>(static_cast<const unsigned*>(flag), value);
+    TSR_CUDA_TRY(cudaGetLastError());
+    return Status::Ok();
+}
+
+Status peer_round_wait(const void* flag_lo, const void* flag_hi, const void* counter,
+                       cudaStream_t s) {
+    round_wait_kernel<<<1, 1, 0, s>>>(static_cast<const unsigned*>(flag_lo),
+                                      static_cast<const unsigned*>(flag_hi),
+                                      static_cast<const unsigned*>(counter));
+    TSR_CUDA_TRY(cudaGetLastError());
+    return Status::Ok();
+}
+
+Status peer_round_signal(void* peer_lo, void* peer_hi, void* counter, cudaStream_t s) {
+    round_signal_kernel<<<1, 1, 0, s>>>(static_cast<unsigned*>(peer_lo),
+                                        static_cast<unsigned*>(peer_hi),
+                                        static_cast<unsigned*>(counter));
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
 }

@@ -272,7 +272,8 @@ class PeerLink:
         self.dist, self.group = dist, group
         self.torch = torch
         self.dg = dg
-        self.flags = torch.zeros(2, dtype=torch.int32, device=dg.device)
+        # [rounds the lo neighbour completed, ... the hi neighbour, rounds I completed]
+        self.flags = torch.zeros(3, dtype=torch.int32, device=dg.device)
         torch.cuda.synchronize(dg.device)
         mine = {"rank": plan.rank, "buf": [_abi.ipc_export(dg.ptr(0)), _abi.ipc_export(dg.ptr(1))],
                 "flags": _abi.ipc_export(self.flags.data_ptr())}
@@ -312,25 +313,25 @@ class PeerLink:
     def _stream(self) -> int:
         return self.torch.cuda.current_stream(self.dg.device).cuda_stream
 
-    def wait(self, rounds_done: int) -> int:
+    def wait(self) -> int:
         """Later work on the current stream waits until both neighbours have
-        completed `rounds_done` rounds.  Returns the kernels launched."""
-        L, n = self._abi.lib(), 0
-        for side, word in (("lo", 0), ("hi", 1)):
-            if side in self.peer:
-                self._abi.check(L.tsr_peer_wait(self.flags.data_ptr() + 4 * word,
-                                                rounds_done & 0xffffffff, self._stream()))
-                n += 1
-        return n
+        completed as many rounds as this rank (the device-side counter), so
+        the call has no per-round arguments and can sit in a CUDA graph.
+        Returns the kernels launched."""
+        f = self.flags.data_ptr()
+        lo = f if "lo" in self.peer else None
+        hi = f + 4 if "hi" in self.peer else None
+        self._abi.check(self._abi.lib().tsr_peer_round_wait(lo, hi, f + 8, self._stream()))
+        return 1
 
-    def signal(self, rounds_done: int) -> int:
-        L, n = self._abi.lib(), 0
-        for side in ("lo", "hi"):
-            if side in self.peer:
-                self._abi.check(L.tsr_peer_signal(self.peer[side]["flag"],
-                                                  rounds_done & 0xffffffff, self._stream()))
-                n += 1
-        return n
+    def signal(self) -> int:
+        """Counts this rank's round and publishes the count to both
+        neighbours (after all earlier work on the stream)."""
+        lo = self.peer["lo"]["flag"] if "lo" in self.peer else None
+        hi = self.peer["hi"]["flag"] if "hi" in self.peer else None
+        self._abi.check(self._abi.lib().tsr_peer_round_signal(lo, hi, self.flags.data_ptr() + 8,
+                                                              self._stream()))
+        return 1
 
     def mirror(self, side: str, which: int) -> tuple[int, int]:
         """(address of the neighbour's buffer `which`, plane shift) for a seam
@@ -354,7 +355,7 @@ class SlabRunner:
     ghost planes with both neighbours, then n fused steps on the local slab."""
 
     def __init__(self, plan: SlabPlan, state, group=None, overlap: bool = True,
-                 transport: str = "nccl"):
+                 transport: str = "nccl", graphs: bool = False):
         import torch.distributed as dist
         if transport not in ("nccl", "peer"):
             raise ValueError("transport must be 'nccl' or 'peer'")
@@ -374,6 +375,11 @@ class SlabRunner:
         self.exchange_bytes = 0
         self.transport = transport
         self.link = None
+        # peer transport: after the first full round, one CUDA graph per
+        # buffer parity is recorded and every later full round replays one
+        self.graphs = graphs
+        self._graph = {}
+        self.graphs_captured = 0
         if transport == "peer" and plan.world > 1:
             if not isinstance(state, _DeviceState):
                 raise ValueError("the peer transport needs device slabs")
@@ -385,13 +391,13 @@ class SlabRunner:
     # -- constructors -----------------------------------------------------
     @classmethod
     def on_device(cls, ts, kernel, plan: SlabPlan, host_local, device, mode="exact",
-                  group=None, overlap=True, transport="nccl"):
+                  group=None, overlap=True, transport="nccl", graphs=False):
         return cls(plan, _DeviceState(ts, kernel, host_local, device, plan.fused_steps, mode),
-                   group, overlap, transport)
+                   group, overlap, transport, graphs)
 
     @classmethod
     def synthetic(cls, ts, kernel, plan: SlabPlan, dtype, device, seed=1, fused_steps=None,
-                  mode="exact", group=None, overlap=True, transport="nccl"):
+                  mode="exact", group=None, overlap=True, transport="nccl", graphs=False):
         """Benchmark slab: the local grid is filled with fill_random(seed)
         directly (no global host grid); the first exchange makes the ghost
         planes consistent with the neighbours."""
@@ -406,7 +412,8 @@ class SlabRunner:
                               plan.halo, esize)
         host = cls_(plan.local_extent, plan.halo)
         ts.fill_random(host, seed)
-        return cls.on_device(ts, kernel, plan, host, device, mode, group, overlap, transport)
+        return cls.on_device(ts, kernel, plan, host, device, mode, group, overlap, transport,
+                             graphs)
 
     @classmethod
     def on_host(cls, plan: SlabPlan, host_local, step_fn, group=None, overlap=False):
@@ -461,14 +468,14 @@ class SlabRunner:
             return (lo, lo), [(lo, hi)]
         return (lo + dl, hi - dh), [(lo, lo + dl), (hi - dh, hi)]
 
-    def _round_peer(self, n: int):
-        """One round over peer memory: interior pass (no wait), wait for the
-        neighbours' previous round, seam passes that also store into the
+    def _peer_launches(self, n: int) -> int:
+        """The GPU work of one peer round (no host-side state changes, so it
+        can be captured): interior pass, wait, seam passes into the
         neighbours' ghost planes, signal."""
         st, link, p = self.state, self.link, self.plan
         (ilo, ihi), seams = self.ranges(n, depth=p.depth)
         launches = st.sweep_range(ilo, ihi, n)
-        launches += link.wait(self.round)
+        launches += link.wait()
         nxt = 1 - st.dg.cur
         first, last = p.ghost_lo, p.ghost_lo + p.own
         # the depth planes each neighbour's ghosts receive
@@ -490,10 +497,46 @@ class SlabRunner:
         for side, a, b in mirrored:
             addr, shift = link.mirror(side, nxt)
             launches += st.sweep_range(a, b, n, mirror=addr, mirror_planes=shift)
-            self.exchange_bytes += p.bytes_per_message
-            self.log.records.append(CommRecord(self.round, f"r{p.rank}_to_{side}",
-                                               p.bytes_per_message))
-        launches += link.signal(self.round + 1)
+        launches += link.signal()
+        return launches
+
+    def _capture(self, cur: int, n: int) -> None:
+        """Records the launches of a full peer round whose current buffer is
+        `cur` into a CUDA graph (recording executes nothing; the buffer
+        index is set for the recording and restored)."""
+        import torch
+        dg = self.state.dg
+        keep = dg.cur
+        dg.cur = cur
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                launches = self._peer_launches(n)
+        finally:
+            dg.cur = keep
+        self._graph[(cur, n)] = (g, launches)
+        self.graphs_captured += 1
+
+    def _round_peer(self, n: int):
+        """One round over peer memory: eager the first time (kernels load),
+        then — with graphs — both buffer parities are recorded once and
+        every later full round is one graph replay."""
+        st, p = self.state, self.plan
+        key = (st.dg.cur, n)
+        if self.graphs and key in self._graph:
+            g, launches = self._graph[key]
+            g.replay()
+        else:
+            launches = self._peer_launches(n)
+            if self.graphs and n == self.fused_steps:
+                for cur in (0, 1):
+                    if (cur, n) not in self._graph:
+                        self._capture(cur, n)
+        for side in ("lo", "hi"):
+            if side in self.link.peer:
+                self.exchange_bytes += p.bytes_per_message
+                self.log.records.append(CommRecord(self.round, f"r{p.rank}_to_{side}",
+                                                   p.bytes_per_message))
         st.flip(n)
 
         class _S:
@@ -558,12 +601,14 @@ class SlabRunner:
 
     def close(self) -> None:
         """Collective teardown of the peer mappings (no-op for NCCL)."""
+        self._graph = {}
         if self.link is not None:
             self.link.close()
             self.link = None
 
     def comm_summary(self) -> dict:
         return {"rounds": self.round, "transport": self.transport if self.plan.world > 1 else None,
+                "graphs_captured": self.graphs_captured,
                 "overlap": bool(self.overlap and self.plan.world > 1),
                 "messages_sent": len(self.log.records),
                 "bytes_per_message": self.plan.bytes_per_message,

@@ -115,7 +115,8 @@ def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, mode):
     loc = local_from_global(glob, plan, poison=True)
     runner = SlabRunner.on_device(ts, kern, plan, loc, torch.device("cuda", 0),
                                   overlap=mode != "serial",
-                                  transport="peer" if mode == "peer" else "nccl")
+                                  transport="peer" if mode.startswith("peer") else "nccl",
+                                  graphs=mode == "peer_graph")
     runner.run(steps)
     runner.close()  # peer transport: every neighbour's stores have landed
     np.save(os.path.join(out_dir, f"own{rank}.npy"), runner.own_rows(loc))
@@ -126,7 +127,7 @@ def _gpu_worker(rank, world, port, name, extent, steps, k, out_dir, mode):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["serial", "overlap", "peer"])
+@pytest.mark.parametrize("mode", ["serial", "overlap", "peer", "peer_graph"])
 @pytest.mark.parametrize("world,name,extent,steps,k", [
     (2, "Heat-3D", [70, 40, 67], 7, 3),   # tb3d engine on each slab
     (3, "Box-2D9P", [90, 130], 9, 4),    # stream2d engine
@@ -139,7 +140,11 @@ def test_slabs_on_device_equal_oracle(ts, orc, tmp_path, world, name, extent, st
     tsr_sweep_range on two streams, zero-copy plane views) with several ranks
     sharing one GPU over gloo; `peer`: the seam passes store straight into the
     neighbour processes' ghost planes through CUDA IPC mappings and the
-    rounds are ordered by device-side flags (no message on the data path)."""
+    rounds are ordered by device-side flags (no message on the data path);
+    `peer_graph`: after the first full round every full round is a replayed
+    CUDA graph (one per buffer parity; a few more rounds so both replay)."""
+    if mode == "peer_graph":
+        steps += 3 * k
     port = _free_port()
     mp.start_processes(_gpu_worker, args=(world, port, name, extent, steps, k, str(tmp_path),
                                           mode),
