@@ -67,6 +67,23 @@ def peaks():
         return HBM_FALLBACK_GBPS, "fallback"
 
 
+# Nominal FP64 / FP32 peaks (148 SMs x 64 FMA lanes x 2 flops x 1.965 GHz; FP32 2x)
+# when profiles/fp_peaks.json (tools/microbench/fp64_peak.cu on a B200) is absent.
+FP_FALLBACK_TFLOPS = {"f64": 37.2, "f32": 74.4}
+
+
+def fp_peak(dtype: str):
+    """Measured FMA throughput of the pool's B200 (ops/s x 2 flops), best over
+    occupancies, from the committed microbenchmark output."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp_peaks.json")) as f:
+            d = json.load(f)
+        key = "dfma" if dtype == "f64" else "ffma"
+        return 2 * max(d["throughput_ops_per_s"][key].values()) / 1e12, "measured"
+    except Exception:
+        return FP_FALLBACK_TFLOPS[dtype], "fallback"
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -348,6 +365,11 @@ def main():
     alg_bytes = 2 * esize * points_per_gpu * kfused
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = ncu_traffic(args.config, kfused)
+    # Arithmetic roofline: the reference's apply_box does one multiply and one
+    # add per tap (naive.hpp:75-78), i.e. 2 * taps algorithmic flops per update.
+    ntaps = len(k.tap_list())
+    fpk, fpk_kind = fp_peak(cfg["dtype"])
+    arith_tflops = 2 * ntaps * points_per_gpu * kfused / (launch_ms / 1e3) / 1e12
 
     e2e = None
     cpu = None
@@ -406,6 +428,14 @@ def main():
                      "basis": (f"algorithmic {2 * esize} B per stencil update x {kfused} fused "
                                f"steps per launch / mean CUDA-event launch time "
                                f"{launch_ms:.4f} ms")},
+        "arith": {"bound": "fp64" if cfg["dtype"] == "f64" else "fp32",
+                  "achieved": round(arith_tflops, 2), "peak": round(fpk, 2), "unit": "TFLOP/s",
+                  "frac": round(arith_tflops / fpk, 4),
+                  "basis": (f"algorithmic {2 * ntaps} flops per update ({ntaps} taps x mul+add,"
+                            f" apply_box) x {kfused} fused steps / mean launch time"),
+                  "peak_source": ("measured FMA rate x 2 (profiles/fp_peaks.json, "
+                                  "tools/microbench/fp64_peak.cu)") if fpk_kind == "measured"
+                  else "nominal 148 SM x 64 FMA x 2 x 1.965 GHz (fp32 2x)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

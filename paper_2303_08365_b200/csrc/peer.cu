@@ -24,6 +24,33 @@ namespace tsr {
 
 namespace {
 
+// A neighbour that never signals (a dead rank, a mapping that does not reach
+// the peer) must fail the stream loudly instead of hanging the device: spins
+// give up after kSpinTimeoutNs of wall time and trap (a sticky launch error
+// the host sees at its next synchronisation).
+constexpr unsigned long long kSpinTimeoutNs = 120ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void spin_until(const unsigned* flag, unsigned value) {
+    const unsigned long long t0 = global_ns();
+    for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (static_cast<int>(v - value) >= 0) return;
+        __nanosleep(200);
+        if (global_ns() - t0 > kSpinTimeoutNs) {
+            printf("tessera_b200: peer flag %p stuck at %u (waiting for %u); trapping\n",
+                   flag, v, value);
+            __trap();
+        }
+    }
+}
+
 __global__ void signal_kernel(unsigned* flag, unsigned value) {
     // every store of earlier work on this stream is complete at kernel
     // boundaries; the fence orders them before the flag for the peer
@@ -31,14 +58,7 @@ __global__ void signal_kernel(unsigned* flag, unsigned value) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
 }
 
-__global__ void wait_kernel(const unsigned* flag, unsigned value) {
-    for (;;) {
-        unsigned v;
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-        if (static_cast<int>(v - value) >= 0) break;
-        __nanosleep(200);
-    }
-}
+__global__ void wait_kernel(const unsigned* flag, unsigned value) { spin_until(flag, value); }
 
 // Round-counting variants (no per-round kernel arguments, so a round can be
 // captured once into a CUDA graph and replayed): `counter` holds the rounds
@@ -47,15 +67,8 @@ __global__ void round_wait_kernel(const unsigned* flag_lo, const unsigned* flag_
                                   const unsigned* counter) {
     unsigned want;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(want) : "l"(counter) : "memory");
-    for (const unsigned* f : {flag_lo, flag_hi}) {
-        if (!f) continue;
-        for (;;) {
-            unsigned v;
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            if (static_cast<int>(v - want) >= 0) break;
-            __nanosleep(200);
-        }
-    }
+    for (const unsigned* f : {flag_lo, flag_hi})
+        if (f) spin_until(f, want);
 }
 
 __global__ void round_signal_kernel(unsigned* peer_lo, unsigned* peer_hi, unsigned* counter) {
