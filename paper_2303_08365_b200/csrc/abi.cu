@@ -317,6 +317,10 @@ struct DeviceCache {
     int64_t bytes = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    // host-layout staging buffer for contiguous device->host copies (lazily
+    // allocated; without it the downloads are pitched 3-D copies)
+    void* stage = nullptr;
+    int64_t stage_bytes = 0;
 };
 std::mutex g_cache_mu;
 std::vector<DeviceCache> g_cache;
@@ -400,13 +404,15 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     const tsr_opts o = opts_or_default(oo);
     if (st) *st = tsr_stats{};
     if (steps == 0) return Status::Ok();
-    if (!halos_equal(g, b0, b1))
-        return Status::Err(TSR_EINVAL,
-                           "halo cells differ between the two buffers (Dirichlet halo must be "
-                           "set in both, as set_both/fill do)");
+    const char* halo_msg =
+        "halo cells differ between the two buffers (Dirichlet halo must be set in both, as "
+        "set_both/fill do)";
     DeviceGuard guard;
     r = guard.enter(o.device);
-    if (!r.ok()) return r;
+    if (!r.ok()) {  // argument errors take precedence over device errors
+        if (!halos_equal(g, b0, b1)) return Status::Err(TSR_EINVAL, halo_msg);
+        return r;
+    }
     int dev = 0;
     TSR_CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(g_cache_mu);
@@ -414,8 +420,25 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     r = cache_for(dev, g.elements * g.esize, &c);
     if (!r.ok()) return r;
     void* host[2] = {b0, b1};
-    r = upload(g, host[parity], c->d[0], c->stream);
+    // PCIe moves one contiguous block per buffer; the pitched device layout
+    // is produced / undone on the device (relayout, ~0.3 ms per GB), which
+    // is 1.4x faster than pitched 3-D copies of 4 KB rows.
+    const int64_t hbytes = g.host_elements * g.esize;
+    const bool staged_up = c->bytes >= hbytes;  // d[1] can hold the host layout
+    if (staged_up) {
+        TSR_CUDA_TRY(cudaMemcpyAsync(c->d[1], host[parity], hbytes, cudaMemcpyHostToDevice,
+                                     c->stream));
+        r = relayout(g, c->d[1], c->d[0], true, c->stream);
+    } else {
+        r = upload(g, host[parity], c->d[0], c->stream);
+    }
     if (!r.ok()) return r;
+    // The host-side precondition check (it touches every page of both
+    // buffers: ~10-20 ms at 512^3) runs while the upload is in flight.
+    if (!halos_equal(g, b0, b1)) {
+        cudaStreamSynchronize(c->stream);
+        return Status::Err(TSR_EINVAL, halo_msg);
+    }
     r = halo_copy(g, c->d[0], c->d[1], c->stream);
     if (!r.ok()) return r;
     int cur = 0;
@@ -425,13 +448,36 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     if (!r.ok()) return r;
     TSR_CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
     const int pfinal = parity ^ static_cast<int>(steps & 1);
-    r = download(g, c->d[cur], host[pfinal], true, c->stream);
+    if (c->stage_bytes < hbytes) {
+        if (c->stage) cudaFree(c->stage);
+        c->stage = nullptr;
+        c->stage_bytes = 0;
+        if (cudaMalloc(&c->stage, hbytes) == cudaSuccess)
+            c->stage_bytes = hbytes;
+        else
+            cudaGetLastError();  // no room: pitched copies below
+    }
+    // The staged path copies the whole host layout back: its halo cells are
+    // the uploaded ones, equal in both host buffers (checked above), so the
+    // host halo is rewritten with its own bytes.
+    auto fetch = [&](int which, int into, int64_t* bytes) -> Status {
+        if (c->stage) {
+            Status q = relayout(g, c->d[which], c->stage, false, c->stream);
+            if (!q.ok()) return q;
+            TSR_CUDA_TRY(cudaMemcpyAsync(host[into], c->stage, hbytes, cudaMemcpyDeviceToHost,
+                                         c->stream));
+            *bytes += hbytes;
+            return Status::Ok();
+        }
+        *bytes += g.interior() * g.esize;
+        return download(g, c->d[which], host[into], true, c->stream);
+    };
+    int64_t d2h = 0;
+    r = fetch(cur, pfinal, &d2h);
     if (!r.ok()) return r;
-    int64_t d2h = g.interior() * g.esize;
     if (steps >= 2) {
-        r = download(g, c->d[1 - cur], host[1 - pfinal], true, c->stream);
+        r = fetch(1 - cur, 1 - pfinal, &d2h);
         if (!r.ok()) return r;
-        d2h *= 2;
     }
     TSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     float ms = 0.f;

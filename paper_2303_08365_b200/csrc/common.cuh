@@ -212,5 +212,9 @@ struct Engine {
 const Engine* find_engine(const Geo& g, const TapSet& t, int* max_fused, int* default_fused);
 
 Status halo_copy(const Geo& g, const void* src, void* dst, cudaStream_t s);
+// Whole padded grid (interior + halo) between the host layout (grid.hpp:46-49,
+// contiguous rows of n2+2h2) and the pitched device layout, device to device:
+// lets tsr_run move a grid over PCIe as one contiguous copy.
+Status relayout(const Geo& g, const void* src, void* dst, bool host_to_device, cudaStream_t s);
 
 }  // namespace tsr

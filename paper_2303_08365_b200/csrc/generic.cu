@@ -110,6 +110,37 @@ __global__ void halo_copy_kernel(const T* __restrict__ src, T* __restrict__ dst,
     }
 }
 
+// One warp per padded row; `src`/`dst` rows start at r0*p0 + r1*p1 + off.
+template <typename T>
+__global__ void relayout_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t rows1,
+                                int64_t rows, int64_t width, int64_t sp0, int64_t sp1,
+                                int64_t soff, int64_t dp0, int64_t dp1, int64_t doff) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        const int64_t r0 = r / rows1, r1 = r - r0 * rows1;
+        const T* s = src + r0 * sp0 + r1 * sp1 + soff;
+        T* d = dst + r0 * dp0 + r1 * dp1 + doff;
+        for (int64_t x = lane; x < width; x += 32) d[x] = s[x];
+    }
+}
+
+template <typename T>
+void relayout_t(const Geo& g, const void* src, void* dst, bool h2d, cudaStream_t s) {
+    const int64_t rows1 = g.n[1] + 2 * g.h[1], rows = g.rows_padded();
+    const int64_t width = g.n[2] + 2 * g.h[2];
+    const int blocks = static_cast<int>(std::min<int64_t>((rows * 32 + 255) / 256, 148 * 16));
+    const int64_t hp0 = g.hpitch[0], hp1 = g.hpitch[1], dp0 = g.pitch[0], dp1 = g.pitch[1];
+    const int64_t doff = g.off2 - g.h[2];
+    if (h2d)
+        relayout_kernel<T><<<blocks, 256, 0, s>>>(static_cast<const T*>(src), static_cast<T*>(dst),
+                                                  rows1, rows, width, hp0, hp1, 0, dp0, dp1, doff);
+    else
+        relayout_kernel<T><<<blocks, 256, 0, s>>>(static_cast<const T*>(src), static_cast<T*>(dst),
+                                                  rows1, rows, width, dp0, dp1, doff, hp0, hp1, 0);
+}
+
 }  // namespace
 
 Status generic_sweep(const LaunchCtx& c, const void* in, void* out, const int64_t lo[3],
@@ -129,6 +160,15 @@ Status halo_copy(const Geo& g, const void* src, void* dst, cudaStream_t s) {
         halo_copy_kernel<float><<<blocks, 256, 0, s>>>(
             static_cast<const float*>(src), static_cast<float*>(dst), g.n[0], g.n[1], g.n[2],
             g.h[0], g.h[1], g.h[2], g.pitch[0], g.pitch[1], g.off2);
+    TSR_CUDA_TRY(cudaGetLastError());
+    return Status::Ok();
+}
+
+Status relayout(const Geo& g, const void* src, void* dst, bool host_to_device, cudaStream_t s) {
+    if (g.dtype == TSR_F64)
+        relayout_t<double>(g, src, dst, host_to_device, s);
+    else
+        relayout_t<float>(g, src, dst, host_to_device, s);
     TSR_CUDA_TRY(cudaGetLastError());
     return Status::Ok();
 }

@@ -400,3 +400,30 @@ def test_reduced_shape_full_steps(ts, orc, cfg):
         ts.run_gpu(fast, k, steps, fused_steps=fused, mode="fast")
         d = ts.deviation(fast, ref)
         assert d["max_rel_deviation"] <= TOL["f32"] and d["l2_rel_err"] <= TOL["f32"]
+
+
+def test_staged_transfers_halo_and_cache_sizes(ts, orc):
+    """tsr_run moves each buffer as one contiguous host-layout block and
+    relayouts it on the device: the host halo comes back with its own bytes
+    (non-zero Dirichlet values, NaN payload included), a halo mismatch between
+    the buffers is still an argument error that leaves the host untouched, and
+    a device cache sized by a larger earlier grid serves a smaller one."""
+    k = ts.find_benchmark("Heat-3D").kernel
+    for extent in ([40, 36, 70], [9, 7, 8], [33, 17, 130]):
+        g = random_grid(ts, orc, extent, [2, 1, 3], 5)
+        for w in (0, 1):
+            p = g.padded(w)
+            p[1, :, :] = 0.75  # halo planes / columns next to the interior
+            p[:, :, -3] = -2.5
+            p[-1, 0, 0] = np.float64("nan")
+        ref = g.copy()
+        ts.run_gpu(g, k, 5)
+        orc.naive_run(ref, k, 5)
+        assert both_buffers_equal(g, ref)
+        assert all(g.padded(w).tobytes() == ref.padded(w).tobytes() for w in (0, 1))
+    g = random_grid(ts, orc, [20, 20, 20], [1, 1, 1], 3)
+    g.buffer(1)[0] = 1.0  # halo differs between the buffers
+    before = [g.buffer(w).tobytes() for w in (0, 1)]
+    with pytest.raises(ValueError, match="halo"):
+        ts.run_gpu(g, k, 3)
+    assert [g.buffer(w).tobytes() for w in (0, 1)] == before and g.parity == 0
