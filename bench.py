@@ -12,11 +12,20 @@ pass stores the r*k boundary planes straight into the neighbours' ghost planes
 over CUDA-IPC peer memory (--transport peer, default) or they are sent with
 NCCL send/recv (--transport nccl).
 
+Arithmetic: Heat-2D/Heat-3D (C1, C3, C5) time FAST mode — one fp64 FMA per
+tap in apply_box's order, admitted by the north star within 1e-12 — and every
+line carries `modes`: the EXACT mode (mul + add per tap, bitwise naive_run)
+timed on the same input, plus the full-grid max_rel_deviation and a bitwise
+flag between the two.  Heat-3D's weights (1/4, 1/8) are powers of two, so its
+products are exact and FAST is bitwise EXACT on normal-range data (the flag
+shows it).  The box kernels (C2, C4) run EXACT: their shared-product Q mode is
+as fast as FMA.
+
 `value` is device-resident throughput (GStencil/s = points * K / time, the
 reference's Eq. 6, proj/src/metrics.cpp:8-20), timed with CUDA events on the
 stream the sweeps launch on, max over ranks.  `e2e` is the same metric through
 the reference-facing call (naive_run on host buffers in pinned memory: H2D of
-the read buffer + K steps + D2H of both buffers' interiors).
+the read buffer + K steps + D2H of both buffers, each one contiguous block).
 `--impl reference` times the reference's own CPU path (oracle/_ref: the
 unmodified reference sources, run_tessellated with all host threads).
 """
@@ -36,14 +45,14 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     "c1": dict(bench="Heat-2D", extent=[4096, 4096], dtype="f64", steps=100, fused=6,
-               mode="exact", workload="C1: 2D heat 5-point star fp64, 4096x4096, 100 timesteps",
+               mode="fast", workload="C1: 2D heat 5-point star fp64, 4096x4096, 100 timesteps",
                ref_tile=[200, 200], ref_tb=50),
     "c2": dict(bench="Box-2D9P", extent=[16384, 16384], dtype="f64", steps=100, fused=4,
                mode="exact",
                workload="C2: 2D 9-point box fp64, 16384x16384, temporal blocking k=4",
                ref_tile=[2000, 2000], ref_tb=4),
     "c3": dict(bench="Heat-3D", extent=[512, 512, 512], dtype="f64", steps=1000, fused=0,
-               mode="exact",
+               mode="fast",
                workload="C3: 3D heat 7-point star fp64, 512^3 per GPU, 1000 timesteps",
                ref_tile=[20, 20, 20], ref_tb=10),
     "c4": dict(bench="Box-3D27P", extent=[1024, 1024, 1024], dtype="f32", steps=100, fused=0,
@@ -52,7 +61,7 @@ CONFIGS = {
                         "(strong scaling), exact mode (shared 1/27 products: bitwise)",
                ref_tile=None, ref_tb=None),
     "c5": dict(bench="Heat-3D", extent=[1024, 1024, 1024], dtype="f64", steps=100, fused=0,
-               mode="exact", workload="C5: 3D heat 7-point fp64, 1024^3 per GPU (weak scaling)",
+               mode="fast", workload="C5: 3D heat 7-point fp64, 1024^3 per GPU (weak scaling)",
                ref_tile=[20, 20, 20], ref_tb=10),
 }
 
@@ -205,6 +214,47 @@ def cpu_baseline(ts, cfg, cfg_name, steps_cap=None):
                       f"slab, T=1"}
 
 
+def mode_check(ts, torch, cfg, k, host, state, per_gpu, dev, stream, kfused, mode, args,
+               total_points, elapsed_ms):
+    """The other arithmetic mode on the same input and step count, timed the
+    same way, and its full-grid deviation from the timed run (max_rel_deviation,
+    metrics.cpp:28-39, and a bitwise flag).  EXACT is apply_box's mul + add
+    per tap (bitwise naive_run); FAST contracts them into one FMA, which the
+    north star admits within 1e-12 (fp64) / 1e-5 (fp32)."""
+    other = "fast" if mode == "exact" else "exact"
+    st2 = ts.DeviceGrid(host, dev)
+    st2.advance(k, 1, fused_steps=kfused, mode=other)  # the timed run's probe step
+    for n in fused_groups(args.warmup, kfused):
+        st2.advance(k, n, fused_steps=kfused, mode=other)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for n in fused_groups(args.steps, kfused):
+        st2.advance(k, n, fused_steps=kfused, mode=other)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms2 = e0.elapsed_time(e1)
+    ext3 = [1] * (3 - len(per_gpu)) + list(per_gpu)
+
+    def interior(s):
+        lay = s.layout
+        return s.buf[s.cur].as_strided(ext3, (lay.pitch[0], lay.pitch[1], 1), lay.origin)
+
+    a, b = interior(state), interior(st2)
+    ref = a if mode == "exact" else b
+    dev_max = float((a.double() - b.double()).abs().max())
+    rel = dev_max / max(1.0, float(ref.double().abs().max()))
+    ival = torch.int64 if a.dtype == torch.float64 else torch.int32
+    bitwise = bool(torch.equal(a.view(ival), b.view(ival)))
+    out = {mode: {"value": round(total_points * args.steps / (elapsed_ms / 1e3) / 1e9, 3)},
+           other: {"value": round(total_points * args.steps / (ms2 / 1e3) / 1e9, 3)},
+           "fast_vs_exact": {"max_rel_deviation": rel, "bitwise_equal": bitwise,
+                             "tolerance": 1e-12 if cfg["dtype"] == "f64" else 1e-5,
+                             "grid": "full interior after warmup + steps"}}
+    del st2
+    return out
+
+
 def run_reference_arm(args, cfg, cfg_name):
     import paper_2303_08365_b200 as ts
     rank = int(os.environ.get("RANK", "0"))
@@ -240,6 +290,8 @@ def main():
     ap.add_argument("--mode", default=None, choices=["exact", "fast"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-mode-check", action="store_true",
+                    help="skip timing the other arithmetic mode and its deviation check")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: exchange, then the whole slab (no interior/seam split)")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
@@ -371,6 +423,11 @@ def main():
     fpk, fpk_kind = fp_peak(cfg["dtype"])
     arith_tflops = 2 * ntaps * points_per_gpu * kfused / (launch_ms / 1e3) / 1e12
 
+    modes = None
+    if world == 1 and not args.no_mode_check:
+        modes = mode_check(ts, torch, cfg, k, host, state, per_gpu, dev, stream, kfused, mode,
+                           args, total_points, elapsed_ms)
+
     e2e = None
     cpu = None
     if rank == 0 and world == 1:
@@ -436,6 +493,7 @@ def main():
                   "peak_source": ("measured FMA rate x 2 (profiles/fp_peaks.json, "
                                   "tools/microbench/fp64_peak.cu)") if fpk_kind == "measured"
                   else "nominal 148 SM x 64 FMA x 2 x 1.965 GHz (fp32 2x)"},
+        "modes": modes,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
