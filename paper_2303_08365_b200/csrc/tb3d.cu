@@ -144,7 +144,7 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 // (q - t_begin) % 3 == s, so the window rotates by renaming (loop unrolled
 // by 3).  a1-neighbour rows of other warps are read two steps after they
 // were written (3-deep SMEM buffers, one __syncthreads per step).
-template <typename T, int K, bool EXACT, int PH, bool SEL, typename G, bool EARLY0, bool MIRROR>
+template <typename T, int K, bool EXACT, int PH, int SEL, typename G, bool EARLY0, bool MIRROR>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
                                           uint64_t* bar, unsigned gbase, int it, int t_begin,
                                           int i0, int i1, int lx, int x, int y, T* obase,
@@ -210,14 +210,18 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                                          Hs[l - 1][sN][cy][1]);
         }
         // Dirichlet: cells outside the interior keep their level-0 value
-        // (only the SEL instantiation, used for edge warps / edge planes).
-        if constexpr (SEL) {
-            const bool pint = p >= 0 && p < a.n0;
+        // (only the SEL instantiations: 1 = boundary columns/rows of this
+        // warp on interior planes, 2 = also a0-boundary planes / wavefront
+        // fill and drain).
+        if constexpr (SEL != 0) {
+            const bool pint = SEL == 1 || (p >= 0 && p < a.n0);
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-                for (int cx = 0; cx < VX; ++cx)
-                    if (!(pint && cint[cy][cx])) res[cy][cx] = Hs[l - 1][sC][cy][cx];
+                for (int cx = 0; cx < VX; ++cx) {
+                    const bool keep = !(pint & cint[cy][cx]);  // one predicate, one select
+                    if (keep) res[cy][cx] = Hs[l - 1][sC][cy][cx];
+                }
         }
         if (l < K) {
             T* L = lev + ((l - 1) * NLEV + sC) * LEV;
@@ -233,14 +237,14 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) Hs[l][sC][cy][cx] = res[cy][cx];
             }
-        } else if (!SEL || (p >= i0 && p < i1)) {  // !SEL: the caller checked the range
+        } else if (SEL != 2 || (p >= i0 && p < i1)) {  // SEL < 2: the caller checked the range
             T* o = obase + (long long)p * a.pitch0;
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy) {
                 T v[VX];
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) v[cx] = fix_zero<EXACT>(res[cy][cx]);
-                if constexpr (!SEL && VX * sizeof(T) == 16) {
+                if constexpr (SEL == 0 && VX * sizeof(T) == 16) {
                     // select-free warps have no boundary column: a lane's two
                     // columns are both in or both out of the output tile
                     if (cout[cy][0]) {
@@ -405,17 +409,24 @@ __global__ void __launch_bounds__(G::NT, 1)
                                                lx, x, y, obase, cint, cout, Hs);                \
     after(IT);
         for (int it = 0; it < niter; it += 3) {
-            if (warp_int && clear(it) && clear(it + 2)) {
-                TB3D_STEP(0, it, false)
-                TB3D_STEP(1, it + 1, false)
-                TB3D_STEP(2, it + 2, false)
+            const bool clr = clear(it) && clear(it + 2);  // implies it + 2 < niter
+            if (warp_int && clr) {
+                TB3D_STEP(0, it, 0)
+                TB3D_STEP(1, it + 1, 0)
+                TB3D_STEP(2, it + 2, 0)
+            } else if (!MIRROR && clr) {  // a2/a1-edge warps of boundary tiles on interior
+                                          // planes (the seam-pass instance keeps two tiers:
+                                          // a third spills it)
+                TB3D_STEP(0, it, 1)
+                TB3D_STEP(1, it + 1, 1)
+                TB3D_STEP(2, it + 2, 1)
             } else {
-                TB3D_STEP(0, it, true)
+                TB3D_STEP(0, it, 2)
                 if (it + 1 < niter) {
-                    TB3D_STEP(1, it + 1, true)
+                    TB3D_STEP(1, it + 1, 2)
                 }
                 if (it + 2 < niter) {
-                    TB3D_STEP(2, it + 2, true)
+                    TB3D_STEP(2, it + 2, 2)
                 }
             }
         }

@@ -109,6 +109,23 @@ def test_heat3d_tuned_bitwise(ts, orc, dt, fused):
         assert halos_equal(a, b)
 
 
+@pytest.mark.parametrize("fused", [1, 2, 3])
+def test_heat3d_fast_is_bitwise_for_power_of_two_weights(ts, orc, fused):
+    """Heat-3D's weights are 1/4 and 1/8: every product is exact on
+    normal-range data, so FAST (one FMA per tap) equals the oracle's mul + add
+    bitwise — the property the bench's fast_vs_exact flag reports at full
+    size.  Covers boundary-tile warps on interior planes (the column-select
+    tier), fill/drain units and a0-boundary planes."""
+    k = ts.find_benchmark("Heat-3D").kernel
+    for extent, halo, steps in [([130, 70, 131], [1, 1, 1], 6), ([64, 61, 190], [1, 2, 1], 9),
+                                ([17, 13, 35], [1, 1, 1], 5)]:
+        a = random_grid(ts, orc, extent, halo, 11, "f64")
+        b = a.copy()
+        ts.run_gpu(a, k, steps, fused_steps=fused, mode="fast", engine="tuned")
+        orc.naive_run(b, k, steps)
+        assert both_buffers_equal(a, b), (extent, steps)
+
+
 def test_star7_general_weights_3d(ts, orc):
     """Non-uniform, non-power-of-two 7-point weights (tap order matters)."""
     w = [((-1, 0, 0), 0.11), ((0, -1, 0), 0.13), ((0, 0, -1), 0.17), ((0, 0, 0), 0.19),
