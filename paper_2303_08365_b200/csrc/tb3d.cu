@@ -408,28 +408,39 @@ __global__ void __launch_bounds__(G::NT, 1)
     tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0, MIRROR>(a, out, ring, lev, bar, gbase, IT, t_begin, i0, i1, \
                                                lx, x, y, obase, cint, cout, Hs);                \
     after(IT);
-        for (int it = 0; it < niter; it += 3) {
-            const bool clr = clear(it) && clear(it + 2);  // implies it + 2 < niter
-            if (warp_int && clr) {
+        // The clear units form one interval of `it` (every condition of
+        // clear() is an interval), so the tier is chosen once per segment:
+        // general units for the wavefront fill, one uniform-tier loop over
+        // the clear middle, general units for the drain.  Tier changes (and
+        // the register moves that join them) happen at most twice per
+        // segment instead of once per unit.
+        auto unit_clear = [&](int it) { return clear(it) && clear(it + 2); };
+        auto general_unit = [&](int it) {
+            TB3D_STEP(0, it, 2)
+            if (it + 1 < niter) {
+                TB3D_STEP(1, it + 1, 2)
+            }
+            if (it + 2 < niter) {
+                TB3D_STEP(2, it + 2, 2)
+            }
+        };
+        int it = 0;
+        for (; it < niter && !unit_clear(it); it += 3) general_unit(it);
+        if (warp_int) {
+            for (; it < niter && unit_clear(it); it += 3) {  // clear implies it + 2 < niter
                 TB3D_STEP(0, it, 0)
                 TB3D_STEP(1, it + 1, 0)
                 TB3D_STEP(2, it + 2, 0)
-            } else if (!MIRROR && clr) {  // a2/a1-edge warps of boundary tiles on interior
-                                          // planes (the seam-pass instance keeps two tiers:
-                                          // a third spills it)
+            }
+        } else if (!MIRROR) {  // a2/a1-edge warps of boundary tiles on interior planes
+                               // (the seam-pass instance keeps two tiers: a third spills it)
+            for (; it < niter && unit_clear(it); it += 3) {
                 TB3D_STEP(0, it, 1)
                 TB3D_STEP(1, it + 1, 1)
                 TB3D_STEP(2, it + 2, 1)
-            } else {
-                TB3D_STEP(0, it, 2)
-                if (it + 1 < niter) {
-                    TB3D_STEP(1, it + 1, 2)
-                }
-                if (it + 2 < niter) {
-                    TB3D_STEP(2, it + 2, 2)
-                }
             }
         }
+        for (; it < niter; it += 3) general_unit(it);
         gbase += niter;
     }
 #undef TB3D_STEP
