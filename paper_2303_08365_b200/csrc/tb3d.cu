@@ -147,7 +147,7 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 template <typename T, int K, bool EXACT, int PH, int SEL, typename G, bool EARLY0, bool MIRROR>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
                                           uint64_t* bar, unsigned gbase, int it, int t_begin,
-                                          int i0, int i1, int lx, int x, int y, T* obase,
+                                          int i0, int i1, int lx, int x, int y, long long& ooff,
                                           const bool (&cint)[G::VY][VX],
                                           const bool (&cout)[G::VY][VX],
                                           T (&Hs)[K][3][G::VY][VX]) {
@@ -238,7 +238,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                 for (int cx = 0; cx < VX; ++cx) Hs[l][sC][cy][cx] = res[cy][cx];
             }
         } else if (SEL != 2 || (p >= i0 && p < i1)) {  // SEL < 2: the caller checked the range
-            T* o = obase + (long long)p * a.pitch0;
+            T* o = out + ooff;  // plane p of this thread's column stack
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy) {
                 T v[VX];
@@ -270,6 +270,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
         Hs[0][PH][cy][0] = v.x;
         Hs[0][PH][cy][1] = v.y;
     }
+    ooff += a.pitch0;
 }
 
 template <typename T, int K, bool EXACT, typename G, bool EARLY0, bool MIRROR>
@@ -357,8 +358,11 @@ __global__ void __launch_bounds__(G::NT, 1)
             }
 
         const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;  // 16-B aligned box start
-        // this thread's output column stack at plane 0 (stores add p * pitch0)
-        T* const obase = out + a.origin + (long long)(gy + y) * a.pitch1 + (gx + x);
+        // element offset of this thread's output column stack at the plane
+        // level K produces in the current step (p = t - 2K), advanced by one
+        // plane per step: stores need no per-step 64-bit index arithmetic
+        long long ooff = a.origin + (long long)(gy + y) * a.pitch1 + (gx + x) +
+                         (long long)(t_begin - 2 * K) * a.pitch0;
         // plane index j (0-based from t_begin) is loaded at most once; the
         // steps that drain the wavefront past the last needed plane (i1+K-1)
         // re-load that plane instead, so a launch never reads outside its
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(G::NT, 1)
         };
 #define TB3D_STEP(PH, IT, SEL)                                                                  \
     tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0, MIRROR>(a, out, ring, lev, bar, gbase, IT, t_begin, i0, i1, \
-                                               lx, x, y, obase, cint, cout, Hs);                \
+                                               lx, x, y, ooff, cint, cout, Hs);                 \
     after(IT);
         // The clear units form one interval of `it` (every condition of
         // clear() is an interval), so the tier is chosen once per segment:
