@@ -146,7 +146,8 @@ __device__ __forceinline__ T stencil7(const T* w, T prev, T up, T left, T c, T r
 // were written (3-deep SMEM buffers, one __syncthreads per step).
 template <typename T, int K, bool EXACT, int PH, int SEL, typename G, bool EARLY0, bool MIRROR>
 __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ out, T* ring, T* lev,
-                                          uint64_t* bar, unsigned gbase, int it, int t_begin,
+                                          uint64_t* bar, int& rslot, unsigned& rphase, int it,
+                                          int t_begin,
                                           int i0, int i1, int lx, int x, int y, long long& ooff,
                                           const bool (&cint)[G::VY][VX],
                                           const bool (&cout)[G::VY][VX],
@@ -157,12 +158,15 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
     constexpr int LEV = lev_bytes<T, G>() / (int)sizeof(T);
     constexpr int BX = BX0<T>, PL = PADL<T>;
     const int t = t_begin + it;
-    const unsigned gi = gbase + it;  // ring loads since kernel start: slot and phase
-    const int slot = gi % STAGES;
+    // ring position of plane t (slot and mbarrier phase), advanced by one per
+    // step instead of divided out of the load count
+    const int slot = rslot;
+    const unsigned phase = rphase;
+    const int slot_m2 = slot >= 2 ? slot - 2 : slot + STAGES - 2;  // plane t-2
     const T* P0 = ring + slot * SLOT;
     P2 early[VY];
     if constexpr (EARLY0) {  // level-0 rows of plane t fetched before the levels' math
-        mbar_wait(&bar[slot], (gi / STAGES) & 1);
+        mbar_wait(&bar[slot], phase);
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
             early[cy] = *reinterpret_cast<const P2*>(P0 + (y + cy + 1) * BX + x + PL);
@@ -178,7 +182,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
         P2 u, d;
         const T* Pm = nullptr;
         if (l == 1) {
-            Pm = ring + ((gi + 2 * STAGES - 2) % STAGES) * SLOT;  // level 0, plane t-2
+            Pm = ring + slot_m2 * SLOT;  // level 0, plane t-2
             u = *reinterpret_cast<const P2*>(Pm + (y) * BX + x + PL);
             d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX + x + PL);
         } else {
@@ -262,7 +266,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
         }
     }
     // Level 0 last: plane t into the window slot level 1 has just consumed.
-    if constexpr (!EARLY0) mbar_wait(&bar[slot], (gi / STAGES) & 1);
+    if constexpr (!EARLY0) mbar_wait(&bar[slot], phase);
 #pragma unroll
     for (int cy = 0; cy < VY; ++cy) {
         const P2 v = EARLY0 ? early[cy]
@@ -271,6 +275,12 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
         Hs[0][PH][cy][1] = v.y;
     }
     ooff += a.pitch0;
+    if (slot == STAGES - 1) {
+        rslot = 0;
+        rphase = phase ^ 1u;
+    } else {
+        rslot = slot + 1;
+    }
 }
 
 template <typename T, int K, bool EXACT, typename G, bool EARLY0, bool MIRROR>
@@ -322,6 +332,8 @@ __global__ void __launch_bounds__(G::NT, 1)
         end = min(pos + a.per_cta, total);
     }
     unsigned gbase = 0;  // ring loads issued by earlier segments
+    int rslot = 0;         // ring slot / mbarrier phase of the next load, i.e.
+    unsigned rphase = 0;   // (gbase + it) % STAGES and ((gbase + it) / STAGES) & 1
     T Hs[K][3][VY][VX];
 #pragma unroll
     for (int l = 0; l < K; ++l)
@@ -385,7 +397,9 @@ __global__ void __launch_bounds__(G::NT, 1)
             // Plane t-2 was last read in this step (level-1 neighbours): its
             // slot takes plane t-2+STAGES.
             if (tid == 0 && it >= 2 && it - 2 + STAGES < niter) {
-                const int sl = (gbase + it - 2) % STAGES;
+                // slot of plane t-2 = (gbase + it - 2) % STAGES; rslot is
+                // already (gbase + it + 1) % STAGES
+                const int sl = rslot + 2 < STAGES ? rslot + 2 : rslot + 2 - STAGES;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&bar[sl], kBoxBytes);
                 tma_load_3d(ring + sl * SLOT, &tmap, &bar[sl], c0, c1,
@@ -409,7 +423,7 @@ __global__ void __launch_bounds__(G::NT, 1)
             return t - 2 * K >= 0 && t - 2 < a.n0 && it >= 3 * K && it < 3 * K + (i1 - i0);
         };
 #define TB3D_STEP(PH, IT, SEL)                                                                  \
-    tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0, MIRROR>(a, out, ring, lev, bar, gbase, IT, t_begin, i0, i1, \
+    tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0, MIRROR>(a, out, ring, lev, bar, rslot, rphase, IT, t_begin, i0, i1, \
                                                lx, x, y, ooff, cint, cout, Hs);                 \
     after(IT);
         // The clear units form one interval of `it` (every condition of
