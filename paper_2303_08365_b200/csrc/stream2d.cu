@@ -170,6 +170,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     const int64_t cone_end = re + (int64_t)K * R; // level-0 rows [t_start, cone_end)
     const T* base_in = in + a.origin + c0;
     T* base_out = out + a.origin + c0;
+    // output row of the current step (level K produces row x = t - K*S),
+    // advanced by one row per step: no 64-bit row multiply per store
+    T* orow = base_out + (t_start - (int64_t)K * S) * a.pitch;
 
     // Fetchable level-0 rows: allocated ([-hrow, rows+hrow)) and inside the
     // cone (< cone_end), for lanes whose columns are allocated; one unsigned
@@ -260,12 +263,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
             } else if (x >= rb && x < re) {
 #pragma unroll
                 for (int v = 0; v < V; ++v) res[v] = fix_zero<EXACT>(res[v]);
-                T* dst = base_out + x * a.pitch;
+                T* dst = orow;
                 store_vals<T, V>(dst, res, cout, all_out);
                 if (a.mirror) store_vals<T, V>(a.mirror + (dst - out) + a.mshift, res, cout, all_out);
             }
         }
         if constexpr (SKEW) level0(PHc);  // row t replaces row t-P, which level 1 has just read
+        orow += a.pitch;
     };
 
     for (int64_t tb = t_start; tb < t_end; tb += P) {
