@@ -165,6 +165,10 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
 
     using V4 = typename VecT<T, 16 / sizeof(T)>::type;
     constexpr int NV = 16 / sizeof(T);
+    // output plane q-1 of step it, advanced by one plane per step (no 64-bit
+    // plane multiply per store)
+    T* orow = out + (a.origin + (long long)(t_begin - 1) * a.pitch0 +
+                     (long long)(gy + y) * a.pitch1 + (gx + x));
     for (int it = 0; it < niter; ++it) {
         const int q = t_begin + it;  // plane in shared memory
         const int slot = it % STAGES;
@@ -201,8 +205,7 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
         apply9<EXACT, false, T, Q>(a.w + 18, nb, accB);
         const int po = q - 1;
         if (it >= 2 && po < i1) {
-            T* o = out + a.origin + (long long)po * a.pitch0 + (long long)(gy + y) * a.pitch1 +
-                   (gx + x);
+            T* o = orow;  // plane po
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy) {
                 store_row<T, VX>(o + cy * a.pitch1, accB[cy], ok[cy]);
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
                     store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, accB[cy], ok[cy]);
             }
         }
+        orow += a.pitch0;
         // output q continues (di = 0), output q+1 starts (di = -1)
         apply9<EXACT, false, T, Q>(a.w + 9, nb, accA);
 #pragma unroll
