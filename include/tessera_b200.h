@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TSR_ABI_VERSION 1
+#define TSR_ABI_VERSION 2
 
 enum tsr_status {
     TSR_OK = 0,
@@ -84,6 +84,10 @@ typedef struct tsr_opts {
     int32_t mode;        /* tsr_mode                                         */
     int32_t engine;      /* tsr_engine                                       */
     int32_t device;      /* CUDA ordinal for tsr_run (-1 = current device)   */
+    int32_t ngpus;       /* tsr_run: slabs / GPUs (0 or 1 = one device); >1
+                            runs tsr_run_multi with an equal split over
+                            devices 0..ngpus-1 (PartitionPlan, scheduler.hpp:49-64) */
+    int32_t split_axis;  /* slab axis; only 0 (the reference's split_axis)  */
 } tsr_opts;
 
 typedef struct tsr_stats {
@@ -96,6 +100,12 @@ typedef struct tsr_stats {
     int64_t d2h_bytes;       /* device->host bytes moved (tsr_run)           */
     int32_t fused_steps;     /* k actually used                              */
     int32_t engine;          /* tsr_engine actually used (1 or 2)            */
+    /* slab runs (CommLog, scheduler.hpp:75-89); zero on one device          */
+    int64_t bytes_exchanged;        /* halo bytes delivered to neighbours    */
+    int64_t messages;               /* per-round seam deliveries             */
+    int64_t ghost_recompute_points; /* HaloWorker::tally_ghost's count       */
+    int32_t ngpus;                  /* slabs the run used                    */
+    int32_t transport;              /* tsr_transport actually used          */
 } tsr_stats;
 
 /* ---- library ---------------------------------------------------------- */
@@ -112,6 +122,11 @@ int tsr_check_kernel(const tsr_kernel* k);
  * buffers, value (T)(lo + (hi-lo) * ((rng()>>11) * 2^-53)). */
 int tsr_fill_random(const tsr_grid* g, void* buf0, void* buf1, uint64_t seed, double lo,
                     double hi);
+/* The same after discarding the first `skip` draws: a slab whose interior is
+ * planes [p, p + n) of a global grid gets the global stream's values with
+ * skip = p * (interior cells per plane). */
+int tsr_fill_random_at(const tsr_grid* g, void* buf0, void* buf1, uint64_t seed, double lo,
+                       double hi, uint64_t skip);
 int tsr_layout_of(const tsr_grid* g, tsr_layout* out);
 
 /* ---- one-call host-buffer path: naive_run / run_tessellated drop-in ---
@@ -190,6 +205,103 @@ int tsr_peer_wait(const void* flag, uint32_t value, void* stream);
 int tsr_peer_round_wait(const void* flag_lo, const void* flag_hi, const void* counter,
                         void* stream);
 int tsr_peer_round_signal(void* peer_lo, void* peer_hi, void* counter, void* stream);
+
+/* ---- memory-level tetrominoes: slab decomposition over GPUs ---------
+ * The reference splits axis 0 between two workers with a deep halo of
+ * r*tb rows and one exchange per direction per tb-step round
+ * (run_heterogeneous, proj/src/scheduler.cpp:441-563; PartitionPlan,
+ * proj/include/tessera/scheduler.hpp:49-64).  Here one host thread drives
+ * `ngpus` slabs, one per GPU (several may share a device), each holding its
+ * owned planes plus r*k ghost planes per seam.  A round of n <= k fused
+ * steps per slab is: seam passes (the r*k boundary planes, storing each
+ * output row locally AND into the neighbour's next-buffer ghost planes over
+ * NVLink peer memory, TSR_XPORT_MIRROR) on one stream, concurrently with the
+ * interior pass on a second stream; ordering across slabs is by CUDA events
+ * (a slab's seam pass of round n waits for its neighbours' of round n-1).
+ * TSR_XPORT_COPY stores locally and moves the planes with
+ * cudaMemcpyPeerAsync (the path when peer access is unavailable). */
+enum tsr_transport { TSR_XPORT_AUTO = 0, TSR_XPORT_MIRROR = 1, TSR_XPORT_COPY = 2 };
+
+typedef struct tsr_partition {
+    int32_t ngpus;              /* slabs (>= 1)                                */
+    int32_t split_axis;         /* must be 0                                   */
+    const int32_t* devices;     /* ngpus CUDA ordinals; NULL = i mod count     */
+    const int64_t* boundaries;  /* ngpus-1 ascending axis-0 boundaries (slab i
+                                   owns [b[i-1], b[i])); NULL = equal split    */
+    int32_t transport;          /* tsr_transport                               */
+    int32_t flags;              /* TSR_PART_POISON: NaN in every slab's
+                                   seam-side halo planes (beyond the ghosts)
+                                   after each upload, proving they are never
+                                   read (run_heterogeneous_instrumented,
+                                   scheduler.hpp:115-124)                     */
+} tsr_partition;
+#define TSR_PART_POISON 1
+
+typedef struct tsr_multi tsr_multi; /* opaque slab set */
+
+typedef struct tsr_slab_info {
+    int32_t device;
+    int32_t cur;           /* buffer holding the current step                */
+    int64_t own_lo, own_hi;/* owned global interior planes [lo, hi)          */
+    int64_t ghost_lo, ghost_hi; /* ghost planes below / above the owned ones */
+    tsr_grid grid;         /* the local slab's geometry                      */
+    tsr_layout layout;     /* its device layout                              */
+    void* buf[2];          /* device buffers                                 */
+} tsr_slab_info;
+
+/* One halo delivery (CommRecord, scheduler.hpp:75-81). */
+typedef struct tsr_comm_record {
+    int64_t round;
+    int32_t from_slab, to_slab;
+    int64_t bytes;         /* depth * interior cross-section * sizeof(T)     */
+    double seam_ms;        /* device time of the sender's seam passes        */
+} tsr_comm_record;
+
+/* Validates the partition (each slab >= r*k planes, the reference's
+ * "subdomain smaller than the halo depth"), enables peer access and
+ * allocates the slabs.  No data is uploaded yet. */
+int tsr_multi_create(const tsr_kernel* k, const tsr_grid* g, const tsr_partition* part,
+                     const tsr_opts* opts, tsr_multi** out);
+int tsr_multi_destroy(tsr_multi* m);
+/* Uploads a whole global host buffer (the reference's layout; its halo is
+ * the Dirichlet boundary) into every slab, ghosts included. */
+int tsr_multi_upload(tsr_multi* m, const void* host);
+/* fill_random(seed, lo, hi) of the GLOBAL grid (random.hpp:20-24: one
+ * std::mt19937_64 stream over the global interior, halo zero), streamed
+ * straight into the slabs through a bounded pinned staging buffer. */
+int tsr_multi_fill_random(tsr_multi* m, uint64_t seed, double lo, double hi);
+/* Advances `steps` time steps (ceil(steps/k) rounds, plus a final one-step
+ * round when keep_previous != 0 so the other buffers hold step T-1).
+ * Synchronous; stats->device_ms is the max over slabs of the CUDA-event time
+ * from a common start (all devices idle) to each slab's last launch. */
+int tsr_multi_advance(tsr_multi* m, int64_t steps, int32_t keep_previous, tsr_stats* stats);
+/* Owned planes of the current buffers -> host_cur, of the other buffers ->
+ * host_prev (NULL = skip); host buffers in the reference's global layout,
+ * other cells untouched. */
+int tsr_multi_download(tsr_multi* m, void* host_cur, void* host_prev);
+int tsr_multi_slab_info(const tsr_multi* m, int32_t slab, tsr_slab_info* out);
+/* Per-round deliveries of the rounds since the last call (records kept only
+ * after tsr_multi_set_logging(m, 1)).  *count = records available; at most
+ * `cap` are copied. */
+int tsr_multi_set_logging(tsr_multi* m, int32_t on);
+int tsr_multi_comm_log(tsr_multi* m, tsr_comm_record* out, int64_t cap, int64_t* count);
+/* A 64-bit position-mixed checksum of every owned global interior plane
+ * (slab axis) of the current (which = 0) or other (which = 1) buffers:
+ * out[p] for p in [0, n0).  Equal planes give equal sums; used to compare a
+ * slab run with a one-device run of the same global grid without moving it. */
+int tsr_multi_plane_checksums(tsr_multi* m, int32_t which, uint64_t* out);
+/* The same checksum over planes [lo, hi) of one device buffer. */
+int tsr_plane_checksums(const tsr_grid* g, const tsr_layout* l, const void* dev, int64_t lo,
+                        int64_t hi, uint64_t* out, void* stream);
+
+/* One-call host-buffer slab run: tsr_run over `part` (NULL = opts->ngpus
+ * equal slabs).  keep_previous != 0: buffers end as naive_run leaves them
+ * (step T and T-1); 0: only buffer(parity ^ (steps&1)) is written, as
+ * run_heterogeneous leaves a grid (it scatters the workers' rows into the
+ * read buffer only, scheduler.cpp:555-557). */
+int tsr_run_multi(const tsr_kernel* k, const tsr_grid* g, void* buf0, void* buf1,
+                  int32_t parity, int64_t steps, const tsr_partition* part,
+                  int32_t keep_previous, const tsr_opts* opts, tsr_stats* stats);
 
 /* Reports the engine (tsr_engine) and fused step count k tsr_advance /
  * tsr_run would use for this kernel, grid and opts (no device work). */

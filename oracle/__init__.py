@@ -44,6 +44,52 @@ def build(ref: bool = True) -> None:
         subprocess.run(["make", "-s", "-j8", "-C", HERE, "ref"], check=True)
 
 
+class HostGrid:
+    """Minimal double-buffered host grid in the reference's own layout
+    (proj/include/tessera/grid.hpp:26-132) for callers that must not import
+    the product: bench.py's reference arm.  Exposes exactly what the
+    checkers below use (extent, halo, dims, dtype, parity, c_buffers,
+    flip_parity, read_data)."""
+
+    def __init__(self, extent, halo, dtype=np.float64):
+        self.extent = [int(e) for e in extent]
+        self.halo = [int(h) for h in halo]
+        self.dims = len(self.extent)
+        self.dtype = np.dtype(dtype).type
+        total = 1
+        for e, h in zip(self.extent, self.halo):
+            total *= e + 2 * h
+        self.parity = 0
+        self._buf = [np.zeros(total, self.dtype), np.zeros(total, self.dtype)]
+
+    def c_buffers(self):
+        return (self._buf[0].ctypes.data, self._buf[1].ctypes.data)
+
+    def flip_parity(self):
+        self.parity ^= 1
+
+    def read_data(self):
+        return self._buf[self.parity]
+
+    def interior_points(self) -> int:
+        n = 1
+        for e in self.extent:
+            n *= e
+        return n
+
+
+class RefKernel:
+    """Tap list of a Table-1 kernel as the reference library defines it
+    (proj/src/bench.cpp:63-85), read through the shim: what the checkers
+    need from a StencilKernel (dims, shape, radius, tap_list)."""
+
+    def __init__(self, ref: "Reference", name: str):
+        self.dims, self.shape, self.radius, self._taps = ref.benchmark_kernel(name)
+
+    def tap_list(self):
+        return list(self._taps)
+
+
 def _geom(grid):
     ext = (ctypes.c_int64 * 3)(*(grid.extent + [1] * (3 - grid.dims)))
     halo = (ctypes.c_int64 * 3)(*(grid.halo + [0] * (3 - grid.dims)))

@@ -16,6 +16,10 @@ from .run import (GpuStats, TilePlan, naive_run, naive_step, plan_tiles, run_gpu
 from .metrics import RateReport, deviation, max_abs, max_rel_deviation, stencils_per_second
 from .device import DeviceGrid, layout_of
 from .harness import csv_header, csv_row, run_all, run_benchmark, write_csv
+from .scheduler import (CommCostModel, CommLog, CommRecord, PartitionPlan, SlabGrid,
+                        WorkerProfile, WorkerSpec, comm_cost, dump_comm_log, plan_partition,
+                        profile_workers, run_heterogeneous, run_heterogeneous_instrumented,
+                        run_multi)
 
 __version__ = "0.1.0"
 
@@ -26,5 +30,7 @@ __all__ = [
     "GpuStats", "TilePlan", "naive_run", "naive_step", "plan_tiles", "run_gpu",
     "run_tessellated", "RateReport", "deviation", "max_abs", "max_rel_deviation",
     "stencils_per_second", "DeviceGrid", "layout_of", "run_benchmark", "run_all", "csv_header",
-    "csv_row", "write_csv",
+    "csv_row", "write_csv", "CommCostModel", "CommLog", "CommRecord", "PartitionPlan",
+    "SlabGrid", "WorkerProfile", "WorkerSpec", "comm_cost", "dump_comm_log", "plan_partition",
+    "profile_workers", "run_heterogeneous", "run_heterogeneous_instrumented", "run_multi",
 ]

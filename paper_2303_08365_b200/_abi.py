@@ -24,11 +24,18 @@ MODES = {"exact": TSR_EXACT, "fast": TSR_FAST}
 # Every symbol include/tessera_b200.h declares (tests check the .so exports them).
 EXPORTED = (
     "tsr_abi_version", "tsr_last_error", "tsr_release_cache", "tsr_check_kernel",
-    "tsr_fill_random", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
+    "tsr_fill_random", "tsr_fill_random_at", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
     "tsr_copy_halo", "tsr_advance", "tsr_query_plan", "tsr_apply_box", "tsr_sweep_range",
     "tsr_sweep_range_mirror", "tsr_ipc_export", "tsr_ipc_open", "tsr_ipc_close",
     "tsr_peer_signal", "tsr_peer_wait", "tsr_peer_round_wait", "tsr_peer_round_signal",
+    "tsr_multi_create", "tsr_multi_destroy", "tsr_multi_upload", "tsr_multi_fill_random",
+    "tsr_multi_advance", "tsr_multi_download", "tsr_multi_slab_info", "tsr_multi_set_logging",
+    "tsr_multi_comm_log", "tsr_multi_plane_checksums", "tsr_plane_checksums", "tsr_run_multi",
 )
+ABI_VERSION = 2
+TSR_XPORT_AUTO, TSR_XPORT_MIRROR, TSR_XPORT_COPY = 0, 1, 2
+TRANSPORTS = {"auto": TSR_XPORT_AUTO, "mirror": TSR_XPORT_MIRROR, "copy": TSR_XPORT_COPY}
+TSR_PART_POISON = 1
 
 
 class TsrKernel(ctypes.Structure):
@@ -65,6 +72,43 @@ class TsrOpts(ctypes.Structure):
         ("mode", ctypes.c_int32),
         ("engine", ctypes.c_int32),
         ("device", ctypes.c_int32),
+        ("ngpus", ctypes.c_int32),
+        ("split_axis", ctypes.c_int32),
+    ]
+
+
+class TsrPartition(ctypes.Structure):
+    _fields_ = [
+        ("ngpus", ctypes.c_int32),
+        ("split_axis", ctypes.c_int32),
+        ("devices", ctypes.POINTER(ctypes.c_int32)),
+        ("boundaries", ctypes.POINTER(ctypes.c_int64)),
+        ("transport", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+    ]
+
+
+class TsrSlabInfo(ctypes.Structure):
+    _fields_ = [
+        ("device", ctypes.c_int32),
+        ("cur", ctypes.c_int32),
+        ("own_lo", ctypes.c_int64),
+        ("own_hi", ctypes.c_int64),
+        ("ghost_lo", ctypes.c_int64),
+        ("ghost_hi", ctypes.c_int64),
+        ("grid", TsrGrid),
+        ("layout", TsrLayout),
+        ("buf", ctypes.c_void_p * 2),
+    ]
+
+
+class TsrCommRecord(ctypes.Structure):
+    _fields_ = [
+        ("round", ctypes.c_int64),
+        ("from_slab", ctypes.c_int32),
+        ("to_slab", ctypes.c_int32),
+        ("bytes", ctypes.c_int64),
+        ("seam_ms", ctypes.c_double),
     ]
 
 
@@ -83,6 +127,11 @@ class TsrStats(ctypes.Structure):
         ("d2h_bytes", ctypes.c_int64),
         ("fused_steps", ctypes.c_int32),
         ("engine", ctypes.c_int32),
+        ("bytes_exchanged", ctypes.c_int64),
+        ("messages", ctypes.c_int64),
+        ("ghost_recompute_points", ctypes.c_int64),
+        ("ngpus", ctypes.c_int32),
+        ("transport", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -114,6 +163,8 @@ def lib() -> ctypes.CDLL:
         L.tsr_check_kernel.argtypes = [p(TsrKernel)]
         L.tsr_fill_random.argtypes = [p(TsrGrid), c_void_p, c_void_p, ctypes.c_uint64,
                                       ctypes.c_double, ctypes.c_double]
+        L.tsr_fill_random_at.argtypes = [p(TsrGrid), c_void_p, c_void_p, ctypes.c_uint64,
+                                         ctypes.c_double, ctypes.c_double, ctypes.c_uint64]
         L.tsr_layout_of.argtypes = [p(TsrGrid), p(TsrLayout)]
         L.tsr_run.argtypes = [p(TsrKernel), p(TsrGrid), c_void_p, c_void_p, ctypes.c_int32,
                               ctypes.c_int64, p(TsrOpts), p(TsrStats)]
@@ -142,10 +193,29 @@ def lib() -> ctypes.CDLL:
         L.tsr_peer_wait.argtypes = [c_void_p, ctypes.c_uint32, c_void_p]
         L.tsr_peer_round_wait.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
         L.tsr_peer_round_signal.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
+        vp = c_void_p
+        L.tsr_multi_create.argtypes = [p(TsrKernel), p(TsrGrid), p(TsrPartition), p(TsrOpts),
+                                       p(vp)]
+        L.tsr_multi_destroy.argtypes = [vp]
+        L.tsr_multi_upload.argtypes = [vp, vp]
+        L.tsr_multi_fill_random.argtypes = [vp, ctypes.c_uint64, ctypes.c_double,
+                                            ctypes.c_double]
+        L.tsr_multi_advance.argtypes = [vp, ctypes.c_int64, ctypes.c_int32, p(TsrStats)]
+        L.tsr_multi_download.argtypes = [vp, vp, vp]
+        L.tsr_multi_slab_info.argtypes = [vp, ctypes.c_int32, p(TsrSlabInfo)]
+        L.tsr_multi_set_logging.argtypes = [vp, ctypes.c_int32]
+        L.tsr_multi_comm_log.argtypes = [vp, p(TsrCommRecord), ctypes.c_int64,
+                                         p(ctypes.c_int64)]
+        L.tsr_multi_plane_checksums.argtypes = [vp, ctypes.c_int32, p(ctypes.c_uint64)]
+        L.tsr_plane_checksums.argtypes = [p(TsrGrid), p(TsrLayout), vp, ctypes.c_int64,
+                                          ctypes.c_int64, p(ctypes.c_uint64), vp]
+        L.tsr_run_multi.argtypes = [p(TsrKernel), p(TsrGrid), vp, vp, ctypes.c_int32,
+                                    ctypes.c_int64, p(TsrPartition), ctypes.c_int32, p(TsrOpts),
+                                    p(TsrStats)]
         for name in EXPORTED:
             if name not in ("tsr_abi_version", "tsr_last_error"):
                 getattr(L, name).restype = ctypes.c_int
-        if L.tsr_abi_version() != 1:
+        if L.tsr_abi_version() != ABI_VERSION:
             raise ImportError("libtessera_b200.so ABI version mismatch")
         _lib = L
         return L
@@ -167,14 +237,43 @@ def check(code: int) -> None:
 
 
 def make_opts(fused_steps: int = 0, mode: str = "exact", engine: str = "auto",
-              device: int = -1) -> TsrOpts:
+              device: int = -1, ngpus: int = 1) -> TsrOpts:
     if mode not in MODES:
         raise ValueError("mode must be 'exact' or 'fast'")
     if engine not in ENGINES:
         raise ValueError("engine must be 'auto', 'generic' or 'tuned'")
     if fused_steps < 0:
         raise ValueError("fused_steps must be >= 0")
-    return TsrOpts(int(fused_steps), MODES[mode], ENGINES[engine], int(device))
+    if ngpus < 1:
+        raise ValueError("ngpus must be >= 1")
+    return TsrOpts(int(fused_steps), MODES[mode], ENGINES[engine], int(device), int(ngpus), 0)
+
+
+def make_partition(ngpus: int, devices=None, boundaries=None, transport: str = "auto",
+                   poison: bool = False):
+    """tsr_partition (arrays kept alive on the returned struct's _keep)."""
+    if transport not in TRANSPORTS:
+        raise ValueError("transport must be 'auto', 'mirror' or 'copy'")
+    part = TsrPartition()
+    part.ngpus = int(ngpus)
+    part.split_axis = 0
+    keep = []
+    if devices is not None:
+        if len(devices) != ngpus:
+            raise ValueError("one device ordinal per slab")
+        arr = (ctypes.c_int32 * ngpus)(*devices)
+        keep.append(arr)
+        part.devices = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32))
+    if boundaries is not None:
+        if len(boundaries) != ngpus - 1:
+            raise ValueError("ngpus - 1 slab boundaries")
+        arr = (ctypes.c_int64 * max(1, ngpus - 1))(*boundaries)
+        keep.append(arr)
+        part.boundaries = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))
+    part.transport = TRANSPORTS[transport]
+    part.flags = TSR_PART_POISON if poison else 0
+    part._keep = keep
+    return part
 
 
 def query_plan(kernel, grid_desc: TsrGrid, fused_steps: int = 0, mode: str = "exact",

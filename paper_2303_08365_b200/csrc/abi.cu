@@ -13,17 +13,14 @@
 #include <sstream>
 #include <vector>
 
-#include "common.cuh"
+#include "runtime.cuh"
 
 namespace tsr {
 
-extern const Engine kStar3dR1Engine;
 extern const Engine kStream2dEngine;
 extern const Engine kTb3dEngine;
 extern const Engine kBox3dEngine;
 extern const Engine kStream1dEngine;
-
-namespace {
 
 thread_local std::string g_last_error;
 
@@ -31,6 +28,8 @@ int report(const Status& s) {
     if (!s.ok()) g_last_error = s.msg;
     return s.code;
 }
+
+namespace {
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -157,8 +156,8 @@ Status check_layout(const Geo& g, const tsr_layout* l) {
 // Tuned engines in preference order.  TSR_ENGINE=<name> (environment) pins
 // one by name for A/B measurements; it never falls back to the CPU.
 const Engine* find_engine(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
-    static const Engine* const engines[] = {&kTb3dEngine, &kBox3dEngine, &kStar3dR1Engine,
-                                            &kStream2dEngine, &kStream1dEngine};
+    static const Engine* const engines[] = {&kTb3dEngine, &kBox3dEngine, &kStream2dEngine,
+                                            &kStream1dEngine};
     const char* pin = std::getenv("TSR_ENGINE");
     for (const Engine* e : engines) {
         if (pin && *pin && std::strcmp(pin, e->name) != 0) continue;
@@ -167,8 +166,6 @@ const Engine* find_engine(const Geo& g, const TapSet& t, int* max_fused, int* de
     return nullptr;
 }
 
-namespace {
-
 Status check_applicable(const Geo& g, const TapSet& t) {
     if (t.dims != g.dims) return Status::Err(TSR_EINVAL, "kernel/grid dimensionality mismatch");
     for (int a = 3 - g.dims; a < 3; ++a)
@@ -176,6 +173,8 @@ Status check_applicable(const Geo& g, const TapSet& t) {
             return Status::Err(TSR_EINVAL, "grid halo too small for kernel radius");
     return Status::Ok();
 }
+
+namespace {
 
 cudaMemcpy3DParms copy_parms(void* dst, int64_t dpitch_el, int64_t dx, int64_t dy, int64_t dz,
                              const void* src, int64_t spitch_el, int64_t sx, int64_t sy,
@@ -191,6 +190,8 @@ cudaMemcpy3DParms copy_parms(void* dst, int64_t dpitch_el, int64_t dx, int64_t d
     p.kind = kind;
     return p;
 }
+
+}  // namespace
 
 Status upload(const Geo& g, const void* host, void* dev, cudaStream_t s) {
     const int64_t ysize = g.n[1] + 2 * g.h[1];
@@ -240,11 +241,6 @@ bool halos_equal(const Geo& g, const void* b0, const void* b1) {
     return true;
 }
 
-struct Plan {
-    const Engine* engine = nullptr;
-    int k = 1;
-};
-
 Status plan_for(const Geo& g, const TapSet& t, const tsr_opts& o, Plan& p) {
     int maxk = 1, defk = 1;
     const Engine* e = nullptr;
@@ -271,6 +267,8 @@ Status sweep(const LaunchCtx& c, const Plan& p, const void* in, void* out, int k
     if (hi[s] <= lo[s]) return Status::Ok();
     return generic_sweep(c, in, out, lo, hi);
 }
+
+namespace {
 
 Status advance(const Geo& g, const TapSet& t, const tsr_opts& o, void* d0, void* d1, int* cur,
                int64_t steps, bool keep_prev, cudaStream_t s, tsr_stats* st) {
@@ -357,26 +355,25 @@ Status cache_for(int dev, int64_t bytes, DeviceCache** out) {
     return Status::Ok();
 }
 
-struct DeviceGuard {
-    int prev = -1;
-    bool set = false;
-    Status enter(int want) {
-        int n = 0;
-        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
-            cudaGetLastError();
-            return Status::Err(TSR_ECUDA, "no CUDA device available to the B200 sweep engine");
-        }
-        TSR_CUDA_TRY(cudaGetDevice(&prev));
-        if (want >= 0 && want != prev) {
-            TSR_CUDA_TRY(cudaSetDevice(want));
-            set = true;
-        }
-        return Status::Ok();
+}  // namespace
+
+Status DeviceGuard::enter(int want) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return Status::Err(TSR_ECUDA, "no CUDA device available to the B200 sweep engine");
     }
-    ~DeviceGuard() {
-        if (set) cudaSetDevice(prev);
+    TSR_CUDA_TRY(cudaGetDevice(&prev));
+    if (want >= 0 && want != prev) {
+        TSR_CUDA_TRY(cudaSetDevice(want));
+        set = true;
     }
-};
+    return Status::Ok();
+}
+
+DeviceGuard::~DeviceGuard() {
+    if (set) cudaSetDevice(prev);
+}
 
 tsr_opts opts_or_default(const tsr_opts* o) {
     if (o) return *o;
@@ -385,8 +382,12 @@ tsr_opts opts_or_default(const tsr_opts* o) {
     d.mode = TSR_EXACT;
     d.engine = TSR_ENGINE_AUTO;
     d.device = -1;
+    d.ngpus = 1;
+    d.split_axis = 0;
     return d;
 }
+
+namespace {
 
 Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, int parity,
                 int64_t steps, const tsr_opts* oo, tsr_stats* st) {
@@ -489,9 +490,13 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     return Status::Ok();
 }
 
+}  // namespace
+
 template <typename T>
-void fill_random_t(const Geo& g, T* b0, T* b1, uint64_t seed, double lo, double hi) {
+void fill_random_t(const Geo& g, T* b0, T* b1, uint64_t seed, double lo, double hi,
+                   uint64_t skip) {
     std::mt19937_64 rng(seed);
+    rng.discard(skip);
     for (int64_t i = 0; i < g.n[0]; ++i)
         for (int64_t j = 0; j < g.n[1]; ++j) {
             const int64_t row = g.horigin + i * g.hpitch[0] + j * g.hpitch[1];
@@ -504,7 +509,14 @@ void fill_random_t(const Geo& g, T* b0, T* b1, uint64_t seed, double lo, double 
         }
 }
 
-}  // namespace
+void fill_random_host(const Geo& g, void* b0, void* b1, uint64_t seed, double lo, double hi,
+                      uint64_t skip) {
+    if (g.dtype == TSR_F64)
+        fill_random_t(g, static_cast<double*>(b0), static_cast<double*>(b1), seed, lo, hi, skip);
+    else
+        fill_random_t(g, static_cast<float*>(b0), static_cast<float*>(b1), seed, lo, hi, skip);
+}
+
 }  // namespace tsr
 
 using namespace tsr;
@@ -518,6 +530,9 @@ Status peer_round_signal(void* peer_lo, void* peer_hi, void* counter, cudaStream
 Status ipc_export(const void* ptr, unsigned char* handle, int64_t* offset);
 Status ipc_open(const unsigned char* handle, void** base);
 Status ipc_close(void* base);
+void release_multi_cache();
+Status run_multi_opts(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b1, int parity,
+                      int64_t steps, const tsr_opts* o, tsr_stats* st);
 }  // namespace tsr
 
 extern "C" {
@@ -527,15 +542,28 @@ int tsr_abi_version(void) { return TSR_ABI_VERSION; }
 const char* tsr_last_error(void) { return g_last_error.c_str(); }
 
 int tsr_release_cache(void) {
+    release_multi_cache();
     std::lock_guard<std::mutex> lock(g_cache_mu);
-    for (DeviceCache& c : g_cache) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (size_t dev = 0; dev < g_cache.size(); ++dev) {
+        DeviceCache& c = g_cache[dev];
+        if (!c.stream && !c.stage && !c.d[0]) continue;
+        cudaSetDevice(static_cast<int>(dev));
         for (void*& p : c.d)
             if (p) {
                 cudaFree(p);
                 p = nullptr;
             }
         c.bytes = 0;
+        if (c.stage) cudaFree(c.stage);
+        c.stage = nullptr;
+        c.stage_bytes = 0;
+        for (cudaEvent_t& e : c.ev)
+            if (e) cudaEventDestroy(e), e = nullptr;
+        if (c.stream) cudaStreamDestroy(c.stream), c.stream = nullptr;
     }
+    cudaSetDevice(prev);
     return TSR_OK;
 }
 
@@ -558,19 +586,23 @@ int tsr_layout_of(const tsr_grid* g, tsr_layout* out) {
 }
 
 int tsr_fill_random(const tsr_grid* g, void* b0, void* b1, uint64_t seed, double lo, double hi) {
+    return tsr_fill_random_at(g, b0, b1, seed, lo, hi, 0);
+}
+
+int tsr_fill_random_at(const tsr_grid* g, void* b0, void* b1, uint64_t seed, double lo,
+                       double hi, uint64_t skip) {
     if (!g || !b0 || !b1) return report(Status::Err(TSR_EINVAL, "null argument"));
     Geo geo;
     Status s = make_geo(*g, geo);
     if (!s.ok()) return report(s);
-    if (geo.dtype == TSR_F64)
-        fill_random_t(geo, static_cast<double*>(b0), static_cast<double*>(b1), seed, lo, hi);
-    else
-        fill_random_t(geo, static_cast<float*>(b0), static_cast<float*>(b1), seed, lo, hi);
+    fill_random_host(geo, b0, b1, seed, lo, hi, skip);
     return TSR_OK;
 }
 
 int tsr_run(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b1, int32_t parity,
             int64_t steps, const tsr_opts* opts, tsr_stats* stats) {
+    if (opts && opts->ngpus > 1)
+        return report(run_multi_opts(k, g, b0, b1, parity, steps, opts, stats));
     return report(run_host(k, g, b0, b1, parity, steps, opts, stats));
 }
 

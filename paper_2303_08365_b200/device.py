@@ -113,6 +113,21 @@ class DeviceGrid:
                 int(mirror_planes), self._stream(stream)))
         return 1
 
+    def plane_checksums(self, which: int = 0, lo: int = 0, hi: int | None = None, stream=None):
+        """64-bit position-mixed checksum of each interior plane [lo, hi) of
+        axis 0 of the current (0) or other (1) buffer (tsr_plane_checksums):
+        compares a grid with a slab run without moving either."""
+        import numpy as np
+        hi = self.extent[0] if hi is None else hi
+        out = np.zeros(max(0, hi - lo), dtype=np.uint64)
+        buf = self.cur if which == 0 else 1 - self.cur
+        with self.torch.cuda.device(self.device):
+            _abi.check(_abi.lib().tsr_plane_checksums(
+                ctypes.byref(self.desc), ctypes.byref(self.layout), self.ptr(buf), int(lo),
+                int(hi), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                self._stream(stream)))
+        return out
+
     def flip(self, steps: int) -> None:
         """Makes the other buffer current after a round of `steps` steps
         written by ``sweep_range`` calls."""
@@ -135,5 +150,7 @@ class DeviceGrid:
             if self.steps_done >= 1 and self.prev_valid:
                 _abi.check(L.tsr_download(ctypes.byref(self.desc), ctypes.byref(self.layout),
                                           self.ptr(1 - self.cur), bufs[1 - grid.parity], 1, s))
-            self.torch.cuda.current_stream(self.device).synchronize()
+            # the copies were queued on `stream` (or the current stream)
+            (stream if stream is not None
+             else self.torch.cuda.current_stream(self.device)).synchronize()
         self.steps_done = 0

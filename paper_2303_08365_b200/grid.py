@@ -186,13 +186,17 @@ def grid_from_numpy(array, halo: Sequence[int] = (), halo_value: float = 0.0,
     return g
 
 
-def fill_random(grid: BasicGrid, seed: int, lo: float = 0.0, hi: float = 1.0) -> None:
+def fill_random(grid: BasicGrid, seed: int, lo: float = 0.0, hi: float = 1.0, *,
+                skip: int = 0) -> None:
     """random.hpp:20-24 (std::mt19937_64, interior only, both buffers), run by
-    the engine library's host code."""
+    the engine library's host code.  `skip` discards that many draws first:
+    a slab holding planes [p, ...) of a global grid gets the global stream's
+    values with skip = p * (interior cells per plane)."""
     L = _abi.lib()
     b0, b1 = grid.c_buffers()
-    _abi.check(L.tsr_fill_random(ctypes.byref(grid.c_struct()), b0, b1,
-                                 ctypes.c_uint64(seed & (2**64 - 1)), float(lo), float(hi)))
+    _abi.check(L.tsr_fill_random_at(ctypes.byref(grid.c_struct()), b0, b1,
+                                    ctypes.c_uint64(seed & (2**64 - 1)), float(lo), float(hi),
+                                    ctypes.c_uint64(int(skip))))
 
 
 # ---- TTRS dump format (proj/src/grid_io.cpp:13-68), fp64 only ---------------

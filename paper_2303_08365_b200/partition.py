@@ -132,18 +132,7 @@ def local_from_global(global_grid, plan: SlabPlan, poison: bool = False):
     return loc
 
 
-@dataclass
-class CommRecord:
-    """scheduler.hpp:75-81."""
-    round: int
-    direction: str
-    bytes: int
-
-
-@dataclass
-class CommLog:
-    records: list = field(default_factory=list)
-    ghost_recompute_points: int = 0
+from .scheduler import CommLog, CommRecord  # noqa: E402  (scheduler.hpp:75-88)
 
 
 class _DeviceState:

@@ -32,18 +32,26 @@ class GpuStats:
     d2h_bytes: int
     fused_steps: int
     engine: str
+    bytes_exchanged: int = 0
+    messages: int = 0
+    ghost_recompute_points: int = 0
+    ngpus: int = 1
+    transport: int = 0
 
 
 def run_gpu(grid: BasicGrid, kernel: StencilKernel, steps: int, *, fused_steps: int = 0,
-            mode: str = "exact", engine: str = "auto", device: int = -1) -> GpuStats:
+            mode: str = "exact", engine: str = "auto", device: int = -1,
+            ngpus: int = 1) -> GpuStats:
     """Advances `grid` by `steps` time steps on the GPU (in place, parity
-    flipped `steps` times, both buffers as naive_run leaves them)."""
+    flipped `steps` times, both buffers as naive_run leaves them).  ngpus > 1
+    splits axis 0 into that many slabs on devices 0..ngpus-1 (modulo the
+    device count), one host thread driving them (tsr_run with opts.ngpus)."""
     steps = int(steps)
     if steps < 0:
         raise ValueError("negative step count")
     L = _abi.lib()
     st = _abi.TsrStats()
-    opts = _abi.make_opts(fused_steps, mode, engine, device)
+    opts = _abi.make_opts(fused_steps, mode, engine, device, ngpus)
     b0, b1 = grid.c_buffers()
     _abi.check(L.tsr_run(ctypes.byref(kernel.c_struct()), ctypes.byref(grid.c_struct()), b0, b1,
                          grid.parity, steps, ctypes.byref(opts), ctypes.byref(st)))
