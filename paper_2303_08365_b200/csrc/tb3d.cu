@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(G::NT, 1)
             // slot takes plane t-2+STAGES.
             if (tid == 0 && it >= 2 && it - 2 + STAGES < niter) {
                 // slot of plane t-2 = (gbase + it - 2) % STAGES; rslot is
-                // already (gbase + it + 1) % STAGES
-                const int sl = rslot + 2 < STAGES ? rslot + 2 : rslot + 2 - STAGES;
+                // already (gbase + it + 1) % STAGES, so the slot is rslot - 3.
+                const int sl = rslot >= 3 ? rslot - 3 : rslot + STAGES - 3;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&bar[sl], kBoxBytes);
                 tma_load_3d(ring + sl * SLOT, &tmap, &bar[sl], c0, c1,

@@ -387,9 +387,10 @@ class SlabRunner:
     @classmethod
     def synthetic(cls, ts, kernel, plan: SlabPlan, dtype, device, seed=1, fused_steps=None,
                   mode="exact", group=None, overlap=True, transport="nccl", graphs=False):
-        """Benchmark slab: the local grid is filled with fill_random(seed)
-        directly (no global host grid); the first exchange makes the ghost
-        planes consistent with the neighbours."""
+        """Benchmark slab: the local grid gets the GLOBAL grid's
+        fill_random(seed) values for its rows (the mt19937_64 stream advanced
+        past the rows below it), without building the global host grid; the
+        ghost rows match the neighbours' from the start."""
         from . import _abi
         cls_ = ts.Grid if dtype == "f64" else ts.GridF
         # resolve the engine's k on the local geometry
@@ -400,7 +401,10 @@ class SlabRunner:
             plan = plan_slabs(plan.global_extent, plan.radius, k, plan.world, plan.rank,
                               plan.halo, esize)
         host = cls_(plan.local_extent, plan.halo)
-        ts.fill_random(host, seed)
+        cross = 1
+        for e in plan.global_extent[1:]:
+            cross *= e
+        ts.fill_random(host, seed, skip=(plan.own_lo - plan.ghost_lo) * cross)
         return cls.on_device(ts, kernel, plan, host, device, mode, group, overlap, transport,
                              graphs)
 

@@ -62,6 +62,12 @@ def run_gpu(grid: BasicGrid, kernel: StencilKernel, steps: int, *, fused_steps: 
     return GpuStats(**d)
 
 
+def release_cache() -> None:
+    """Frees the device buffers and staging memory tsr_run / tsr_run_multi
+    keep between calls (tsr_release_cache)."""
+    _abi.check(_abi.lib().tsr_release_cache())
+
+
 def naive_step(grid: BasicGrid, kernel: StencilKernel) -> None:
     """naive.hpp:89-94 on the GPU."""
     run_gpu(grid, kernel, 1)
