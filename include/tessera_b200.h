@@ -127,6 +127,12 @@ int tsr_fill_random(const tsr_grid* g, void* buf0, void* buf1, uint64_t seed, do
  * skip = p * (interior cells per plane). */
 int tsr_fill_random_at(const tsr_grid* g, void* buf0, void* buf1, uint64_t seed, double lo,
                        double hi, uint64_t skip);
+/* The thermal case study's initial plate (proj/src/case_study.cpp:193-207):
+ * ambient everywhere, interior cell (i, j) = ambient + (peak - ambient) *
+ * exp(-((i-c0)^2 + (j-c0)^2) / (2 sigma^2)), c0 = (n-1)/2 per axis, computed
+ * in double (std::exp) and cast to the grid type; both buffers; 2-D only. */
+int tsr_fill_plate(const tsr_grid* g, void* buf0, void* buf1, double ambient, double peak,
+                   double sigma);
 int tsr_layout_of(const tsr_grid* g, tsr_layout* out);
 
 /* ---- one-call host-buffer path: naive_run / run_tessellated drop-in ---

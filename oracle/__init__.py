@@ -255,3 +255,31 @@ class Reference:
         if p != grid.parity:
             grid.flip_parity()
         return log[0], log[1], log[2], bnd.value
+
+    def case_study_heat(self, out_dir: str, extent: int, steps: int, checkpoints, sample_every: int,
+                        mu: float = 0.23, sigma: float = 0.0, path: str = "tessellate",
+                        threads: int = 1) -> dict:
+        """The reference's case_study_heat (case_study.cpp:171-290), run by
+        _ref/case_study_ref in its own process: its artifacts in out_dir and
+        the result arrays (bit-exact, via hex floats)."""
+        exe = os.path.join(HERE, "_ref", "case_study_ref")
+        out = subprocess.run([exe, out_dir, str(extent), str(steps), str(sample_every),
+                              repr(float(mu)), repr(float(sigma)), path, str(threads),
+                              ",".join(str(int(c)) for c in checkpoints)],
+                             capture_output=True, text=True)
+        if out.returncode != 0:
+            raise ValueError(out.stderr.strip())
+        res = {"series_steps": [], "center_series": [], "checkpoint_steps": [],
+               "checkpoint_errors": [], "final_center": None}
+        for line in out.stdout.splitlines():
+            tok = line.split()
+            if tok[0] == "series":
+                res["series_steps"].append(int(tok[1]))
+                res["center_series"].append(float.fromhex(tok[2]))
+            elif tok[0] == "check":
+                v = [float.fromhex(t) for t in tok[2:8]]
+                res["checkpoint_steps"].append(int(tok[1]))
+                res["checkpoint_errors"].append((v[:3], v[3:]))
+            elif tok[0] == "final":
+                res["final_center"] = float.fromhex(tok[1])
+        return res

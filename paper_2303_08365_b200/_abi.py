@@ -24,7 +24,7 @@ MODES = {"exact": TSR_EXACT, "fast": TSR_FAST}
 # Every symbol include/tessera_b200.h declares (tests check the .so exports them).
 EXPORTED = (
     "tsr_abi_version", "tsr_last_error", "tsr_release_cache", "tsr_check_kernel",
-    "tsr_fill_random", "tsr_fill_random_at", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
+    "tsr_fill_random", "tsr_fill_random_at", "tsr_fill_plate", "tsr_layout_of", "tsr_run", "tsr_upload", "tsr_download",
     "tsr_copy_halo", "tsr_advance", "tsr_query_plan", "tsr_apply_box", "tsr_sweep_range",
     "tsr_sweep_range_mirror", "tsr_ipc_export", "tsr_ipc_open", "tsr_ipc_close",
     "tsr_peer_signal", "tsr_peer_wait", "tsr_peer_round_wait", "tsr_peer_round_signal",
@@ -165,6 +165,8 @@ def lib() -> ctypes.CDLL:
                                       ctypes.c_double, ctypes.c_double]
         L.tsr_fill_random_at.argtypes = [p(TsrGrid), c_void_p, c_void_p, ctypes.c_uint64,
                                          ctypes.c_double, ctypes.c_double, ctypes.c_uint64]
+        L.tsr_fill_plate.argtypes = [p(TsrGrid), c_void_p, c_void_p, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double]
         L.tsr_layout_of.argtypes = [p(TsrGrid), p(TsrLayout)]
         L.tsr_run.argtypes = [p(TsrKernel), p(TsrGrid), c_void_p, c_void_p, ctypes.c_int32,
                               ctypes.c_int64, p(TsrOpts), p(TsrStats)]

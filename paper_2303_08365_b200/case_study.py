@@ -15,7 +15,7 @@ reference would print.
 """
 from __future__ import annotations
 
-import math
+import ctypes
 import os
 import time
 from dataclasses import dataclass, field
@@ -137,16 +137,14 @@ def parse_case_config(path: str) -> CaseStudyConfig:
 
 
 def _init(grid, cfg: CaseStudyConfig, sigma: float) -> None:
-    """Interior Gaussian over a cold-ambient Dirichlet rim (case_study.cpp:193-207)."""
-    n = cfg.extent
-    c0 = (n - 1) / 2.0
-    idx = np.arange(n, dtype=np.float64) - c0
-    r2 = idx[:, None] ** 2 + idx[None, :] ** 2
-    field_ = cfg.ambient_celsius + (cfg.peak_celsius - cfg.ambient_celsius) * np.exp(
-        -r2 / (2.0 * sigma * sigma))
-    grid.fill(cfg.ambient_celsius)
-    for w in (0, 1):
-        grid.interior_view(w)[...] = field_.astype(grid.dtype)
+    """Interior Gaussian over a cold-ambient Dirichlet rim, both buffers
+    (case_study.cpp:193-207), evaluated by the engine library's host code
+    with std::exp in double and cast to the grid type, as the reference does
+    (tsr_fill_plate), so the initial fields are bit-identical to its own."""
+    b0, b1 = grid.c_buffers()
+    _abi.check(_abi.lib().tsr_fill_plate(ctypes.byref(grid.c_struct()), b0, b1,
+                                         float(cfg.ambient_celsius), float(cfg.peak_celsius),
+                                         float(sigma)))
 
 
 def case_study_heat(cfg: CaseStudyConfig, out_dir: str | None = None, device=None) -> dict:
@@ -213,26 +211,37 @@ def case_study_heat(cfg: CaseStudyConfig, out_dir: str | None = None, device=Non
     res["fp32_gstencil_s"] = pts / t32 / 1e9 if t32 > 0 else 0.0
     if out_dir:
         os.makedirs(out_dir, exist_ok=True)
+        # the final fp64 field, always (case_study.cpp:241-242)
+        if not res["checkpoint_steps"] or res["checkpoint_steps"][-1] != done:
+            final = Grid([n, n], [1, 1])
+            _init(final, cfg, sigma)
+            d64.download(final)
+            fp64 = final
+        dump_grid(os.path.join(out_dir, "final.ttrs"), fp64)
+        res["artifacts"].append(os.path.join(out_dir, "final.ttrs"))
+        # the reference's CSV headers and C++ ostream number format (%g)
         with open(os.path.join(out_dir, "center_series.csv"), "w") as f:
-            f.write("step,center_celsius\n")
+            f.write("step,center_c\n")
             for s, c in zip(res["series_steps"], res["center_series"]):
-                f.write(f"{s},{c!r}\n")
+                f.write(f"{s},{c:g}\n")
         with open(os.path.join(out_dir, "error_table.csv"), "w") as f:
-            f.write("step,abs_gt_0.1,abs_gt_0.5,abs_gt_1.0,rel_gt_1pct,rel_gt_3pct,rel_gt_5pct\n")
+            f.write("T,abs_gt_0.1,abs_gt_0.5,abs_gt_1.0,rel_gt_1pct,rel_gt_3pct,rel_gt_5pct\n")
             for s, t in zip(res["checkpoint_steps"], res["checkpoint_errors"]):
-                f.write(f"{s}," + ",".join(f"{v:.4f}" for v in t.abs_exceed_pct + t.rel_exceed_pct)
+                f.write(f"{s}," + ",".join(f"{v:g}" for v in t.abs_exceed_pct + t.rel_exceed_pct)
                         + "\n")
-        if res["checkpoint_steps"] and res["checkpoint_steps"][-1] == cfg.steps:
-            dump_grid(os.path.join(out_dir, "final.ttrs"), fp64)
-            res["artifacts"].append(os.path.join(out_dir, "final.ttrs"))
         with open(os.path.join(out_dir, "metadata.txt"), "w") as f:
-            f.write(f"extent = {n}\nsteps = {cfg.steps}\nmu = {cfg.mu}\nsigma_cells = {sigma}\n"
-                    f"peak_celsius = {cfg.peak_celsius}\nambient_celsius = {cfg.ambient_celsius}\n"
-                    f"final_center_celsius = {res['final_center']!r}\n"
+            f.write(f"plate_side_mm = {cfg.plate_side_mm:g}\nmu = {cfg.mu:g}\n"
+                    f"extent = {n}x{n}\nsteps = {cfg.steps}\ninitial = gaussian\n"
+                    f"gaussian_peak_c = {cfg.peak_celsius:g}\n"
+                    f"gaussian_sigma_cells = {sigma:g}\n"
+                    f"ambient_c = {cfg.ambient_celsius:g}\nboundary = dirichlet ambient\n"
+                    f"path = gpu ({cfg.mode} mode, fused_steps {cfg.fused_steps or 'auto'})\n"
+                    f"fp32_twin = B200 exact mode (bitwise the reference executor's "
+                    f"32-bit arithmetic)\n"
+                    f"final_center_c = {res['final_center']!r}\n"
                     f"fp64_device_s = {t64:.3f}\nfp32_device_s = {t32:.3f}\n"
                     f"fp64_gstencil_s = {res['fp64_gstencil_s']:.2f}\n"
-                    f"fp32_gstencil_s = {res['fp32_gstencil_s']:.2f}\n"
-                    f"mode = {cfg.mode}\n")
+                    f"fp32_gstencil_s = {res['fp32_gstencil_s']:.2f}\n")
         res["artifacts"] += [os.path.join(out_dir, x) for x in
                              ("center_series.csv", "error_table.csv", "metadata.txt")]
     return res

@@ -517,6 +517,30 @@ void fill_random_host(const Geo& g, void* b0, void* b1, uint64_t seed, double lo
         fill_random_t(g, static_cast<float*>(b0), static_cast<float*>(b1), seed, lo, hi, skip);
 }
 
+// The case study's plate (proj/src/case_study.cpp:193-207): every cell of
+// both buffers is the ambient temperature except the interior, which holds
+// ambient + (peak - ambient) * exp(-(di^2 + dj^2) / (2 sigma^2)) around the
+// plate centre c0 = (n - 1) / 2, evaluated in double with std::exp and then
+// cast to T, exactly as the reference's init_temp / initialize do.  (Host
+// code: x86-64 without -mfma, so nothing is contracted into an FMA.)
+template <typename T>
+void fill_plate_t(const Geo& g, T* b0, T* b1, double ambient, double peak, double sigma) {
+    const int64_t rows = g.n[1] + 2 * g.h[1], cols = g.n[2] + 2 * g.h[2];
+    const double ci = static_cast<double>(g.n[1] - 1) / 2.0;
+    const double cj = static_cast<double>(g.n[2] - 1) / 2.0;
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t c = 0; c < cols; ++c) {
+            const int64_t i = r - g.h[1], j = c - g.h[2];
+            double v = ambient;
+            if (i >= 0 && i < g.n[1] && j >= 0 && j < g.n[2]) {
+                const double di = static_cast<double>(i) - ci, dj = static_cast<double>(j) - cj;
+                v = ambient + (peak - ambient) * std::exp(-(di * di + dj * dj) / (2.0 * sigma * sigma));
+            }
+            b0[r * g.hpitch[1] + c] = static_cast<T>(v);
+            b1[r * g.hpitch[1] + c] = static_cast<T>(v);
+        }
+}
+
 }  // namespace tsr
 
 using namespace tsr;
@@ -596,6 +620,21 @@ int tsr_fill_random_at(const tsr_grid* g, void* b0, void* b1, uint64_t seed, dou
     Status s = make_geo(*g, geo);
     if (!s.ok()) return report(s);
     fill_random_host(geo, b0, b1, seed, lo, hi, skip);
+    return TSR_OK;
+}
+
+int tsr_fill_plate(const tsr_grid* g, void* b0, void* b1, double ambient, double peak,
+                   double sigma) {
+    if (!g || !b0 || !b1) return report(Status::Err(TSR_EINVAL, "null argument"));
+    Geo geo;
+    Status s = make_geo(*g, geo);
+    if (!s.ok()) return report(s);
+    if (geo.dims != 2) return report(Status::Err(TSR_EINVAL, "the plate is a 2-D grid"));
+    if (!(sigma > 0.0)) return report(Status::Err(TSR_EINVAL, "sigma must be positive"));
+    if (geo.dtype == TSR_F64)
+        fill_plate_t(geo, static_cast<double*>(b0), static_cast<double*>(b1), ambient, peak, sigma);
+    else
+        fill_plate_t(geo, static_cast<float*>(b0), static_cast<float*>(b1), ambient, peak, sigma);
     return TSR_OK;
 }
 

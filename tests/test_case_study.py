@@ -35,29 +35,62 @@ def test_config_validation(ts):
         case_study_heat(CaseStudyConfig(steps=100, checkpoints=[30], sample_every=25))
 
 
+def test_initial_plate_is_the_references(ts, ref, tmp_path):
+    """The initial field (case_study.cpp:193-207, std::exp in double) is
+    bit-identical to the reference's: its case_study_heat with 0 steps dumps
+    the untouched plate as final.ttrs."""
+    from paper_2303_08365_b200.case_study import CaseStudyConfig, _init
+    for n, sigma in [(96, 0.0), (101, 7.5)]:
+        out = tmp_path / f"ref{n}"
+        ref.case_study_heat(str(out), n, 0, [], 25, sigma=sigma)
+        g = ts.Grid([n, n], [1, 1])
+        _init(g, CaseStudyConfig(extent=n), sigma if sigma > 0 else n / 8.0)
+        ts.dump_grid(str(tmp_path / f"ours{n}.ttrs"), g)
+        assert (tmp_path / f"ours{n}.ttrs").read_bytes() == (out / "final.ttrs").read_bytes()
+        assert g.buffer(0).tobytes() == g.buffer(1).tobytes()
+        f = ts.GridF([n, n], [1, 1])
+        _init(f, CaseStudyConfig(extent=n), sigma if sigma > 0 else n / 8.0)
+        assert f.buffer(0).tobytes() == g.buffer(0).astype(np.float32).tobytes()
+
+
+def _check_against_reference(ts, ref, cfg, tmp_path, threads=1):
+    from paper_2303_08365_b200.case_study import case_study_heat
+    res = case_study_heat(cfg, str(tmp_path / "ours"))
+    want = ref.case_study_heat(str(tmp_path / "ref"), cfg.extent, cfg.steps, cfg.checkpoints,
+                               cfg.sample_every, mu=cfg.mu, path="tessellate", threads=threads)
+    assert res["series_steps"] == want["series_steps"]
+    assert res["center_series"] == want["center_series"]  # bitwise
+    assert res["final_center"] == want["final_center"]
+    assert res["checkpoint_steps"] == want["checkpoint_steps"]
+    for got, (wa, wr) in zip(res["checkpoint_errors"], want["checkpoint_errors"]):
+        assert got.abs_exceed_pct == wa and got.rel_exceed_pct == wr
+    ours, theirs = tmp_path / "ours", tmp_path / "ref"
+    assert (ours / "final.ttrs").read_bytes() == (theirs / "final.ttrs").read_bytes()
+    for name in ("center_series.csv", "error_table.csv"):
+        assert (ours / name).read_text() == (theirs / name).read_text(), name
+    return res
+
+
 @pytest.mark.gpu
-def test_small_study_matches_oracle(ts, orc, tmp_path):
-    from paper_2303_08365_b200.case_study import (CaseStudyConfig, _init, case_study_heat,
-                                                  compare_precision)
+def test_small_study_matches_reference(ts, ref, tmp_path):
+    """case_study_heat on the GPU against the reference's own case_study_heat
+    (tessellate path): centre series, exceedance tables, final.ttrs and the
+    two CSVs, all identical."""
+    from paper_2303_08365_b200.case_study import CaseStudyConfig
     cfg = CaseStudyConfig(extent=96, steps=300, checkpoints=[100, 300], sample_every=50)
-    res = case_study_heat(cfg, str(tmp_path))
-    k = ts.heat_coefficients(cfg.mu)
-    g64, g32 = ts.Grid([96, 96], [1, 1]), ts.GridF([96, 96], [1, 1])
-    _init(g64, cfg, 96 / 8.0)
-    _init(g32, cfg, 96 / 8.0)
-    centers, tables = [g64.at(48, 48)], []
-    for done in range(50, 301, 50):
-        orc.naive_run(g64, k, 50)
-        orc.naive_run(g32, k, 50)
-        centers.append(g64.at(48, 48))
-        if done in (100, 300):
-            tables.append(compare_precision(g64, g32))
-    assert res["series_steps"] == list(range(0, 301, 50))
-    assert res["center_series"] == [float(c) for c in centers]  # bitwise
-    assert res["checkpoint_steps"] == [100, 300]
-    for got, want in zip(res["checkpoint_errors"], tables):
-        assert got.abs_exceed_pct == want.abs_exceed_pct
-        assert got.rel_exceed_pct == want.rel_exceed_pct
-    final = ts.load_grid(str(tmp_path / "final.ttrs"))
-    assert final.to_numpy().tobytes() == g64.to_numpy().tobytes()
-    assert (tmp_path / "center_series.csv").read_text().startswith("step,center_celsius")
+    _check_against_reference(ts, ref, cfg, tmp_path)
+    # final step off the checkpoint list: final.ttrs is still written
+    cfg = CaseStudyConfig(extent=64, steps=130, checkpoints=[50], sample_every=25)
+    _check_against_reference(ts, ref, cfg, tmp_path / "b")
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_desk_scale_study_matches_reference(ts, ref, tmp_path):
+    """The reference's default desk-scale study (480 x 480, 9500 steps,
+    checkpoints 1000/5000/9500), identical end to end."""
+    import os
+    from paper_2303_08365_b200.case_study import CaseStudyConfig
+    res = _check_against_reference(ts, ref, CaseStudyConfig(), tmp_path,
+                                   threads=os.cpu_count() or 1)
+    assert len(res["center_series"]) == 9500 // 25 + 1

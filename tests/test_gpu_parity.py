@@ -20,6 +20,17 @@ def both_buffers_equal(a, b):
             a.interior_view(1).tobytes() == b.interior_view(1).tobytes())
 
 
+def both_buffers_equal_planes(a, b):
+    """both_buffers_equal one axis-0 plane at a time (no full-grid copies)."""
+    if a.parity != b.parity:
+        return False
+    for w in (0, 1):
+        x, y = a.interior_view(w), b.interior_view(w)
+        if any(x[i].tobytes() != y[i].tobytes() for i in range(x.shape[0])):
+            return False
+    return True
+
+
 def halos_equal(a, b):
     mask = np.ones(a.padded(0).shape, bool)
     mask[tuple(slice(h, h + e) for e, h in zip(a.extent, a.halo))] = False
@@ -295,6 +306,37 @@ def test_full_shape_properties(ts, orc, cfg):
     ts.run_gpu(c, k, 2, fused_steps=fused, mode="exact")
     orc.naive_run(d, k, 2)
     assert both_buffers_equal(c, d)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_shape_1024(ts, orc, cfg):
+    """C4 (Box-3D27P fp32) and C5 (Heat-3D fp64) at their full 1024^3 shape:
+    the tuned engine at its default fused depth == the generic engine bitwise
+    for k + 1 steps (EXACT), and 2 steps == the oracle bitwise."""
+    import gc
+    name, dt = {"c4": ("Box-3D27P", "f32"), "c5": ("Heat-3D", "f64")}[cfg]
+    k = ts.find_benchmark(name).kernel
+    cls = ts.Grid if dt == "f64" else ts.GridF
+    ext = [1024, 1024, 1024]
+    a = cls(ext, [1, 1, 1])
+    ts.fill_random(a, 1)
+    b = a.copy()
+    st = ts.run_gpu(a, k, 1, mode="exact")
+    kf = st.fused_steps
+    ts.run_gpu(a, k, kf + 1, fused_steps=kf, mode="exact")
+    ts.run_gpu(b, k, kf + 2, engine="generic", mode="exact")
+    assert both_buffers_equal_planes(a, b), f"tuned k={kf} != generic"
+    del a, b
+    gc.collect()
+    ts.release_cache()
+    c = cls(ext, [1, 1, 1])
+    ts.fill_random(c, 1)
+    d = c.copy()
+    ts.run_gpu(c, k, 2, mode="exact")
+    orc.naive_run(d, k, 2)
+    assert both_buffers_equal_planes(c, d)
+    ts.release_cache()
 
 
 @pytest.mark.parametrize("name,extent,fused,dt", [

@@ -161,3 +161,19 @@ def test_deviation_metric(ts, orc):
     assert d["max_rel_deviation"] == pytest.approx(0.5)
     assert d == pytest.approx({k: v for k, v in ts.deviation(b, a).items()
                                if k != "bitwise_equal"})
+
+
+@pytest.mark.parametrize("name,extent,dt", [("Heat-3D", [120, 100, 96], "f64"),
+                                            ("Box-3D27P", [100, 110, 97], "f32"),
+                                            ("Box-2D9P", [1200, 1100], "f64")])
+def test_threaded_oracle_matches_reference(ts, orc, ref, name, extent, dt):
+    """Boxes above 2^20 points run the oracle's row-split host threads; the
+    result stays bitwise the reference's serial naive_run."""
+    k = ts.find_benchmark(name).kernel
+    a = random_grid(ts, orc, extent, [1] * len(extent), 9, dt)
+    b = a.copy()
+    orc.naive_run(a, k, 3)
+    ref.naive_run(b, k, 3)
+    assert a.parity == b.parity
+    for w in (0, 1):
+        assert a.interior_view(w).tobytes() == b.interior_view(w).tobytes()

@@ -10,7 +10,7 @@ for item in "${S[@]}"; do
   cfg=${item%%:*}; args=${item#*:}
   timeout 300 python bench.py --no-cpu --no-e2e --config $cfg $args 2>>gpurun_out/sweep.err | tee -a gpurun_out/sweep.jsonl | python -c "import json,sys
 try:
- d=json.loads(sys.stdin.read()); print('$cfg $args', d['value'], d['roofline']['frac'], d['config']['engine'], d['config']['fused_steps'], d['ms_per_step'], d['clocks']['sm_mhz'], d['clocks']['reasons'])
+ d=json.loads(sys.stdin.read()); print('$cfg $args', d['value'], d['roofline']['frac'], d['plan']['engine'], d['plan']['fused_steps'], d['ms_per_step'], d['clocks']['sm_mhz'], d['clocks']['reasons'])
 except Exception as e: print('$cfg $args FAILED', e)"
 done
 IFS=';' read -ra N <<< "$NCU"
