@@ -1,14 +1,17 @@
 // tb3d.cu — 3-D radius-1 star (7-point) sweep with K time steps fused per
 // HBM pass: the paper's three tiers rebuilt for sm_100a.
 //
-//  * Memory tier: a CTA owns an output tile of (32-2(K-1)) x (64-2(K-1))
-//    cells of the (a1, a2) plane and streams consecutive a0 planes of it;
-//    for K >= 2 the grid is persistent (one CTA per SM, each an equal share
-//    of the (tile, plane) positions, so the wavefront refills only when a
-//    CTA moves to its next tile).  Level-0
-//    planes (the tile plus a (K-1)+1 halo ring) arrive by TMA
-//    (cp.async.bulk.tensor.3d) into a 5-stage shared-memory ring guarded by
-//    mbarriers (planes t-2 .. t+2 of step t).
+//  * Memory tier: a CTA owns an output tile of (R1Y-2(K-1)) x (64-2(K-1))
+//    cells of the (a1, a2) plane (region R1Y = 32, or 36 for K = 3) and
+//    streams consecutive a0 planes of it.  For K >= 2 the grid is
+//    persistent, one CTA per SM: CTA b streams whole tiles b, b+W, ... with
+//    every CTA at the same plane, so neighbouring tiles read the halo rows
+//    their boxes share once from HBM and once from L2 (C3: 2.86 -> 2.29 GB
+//    of DRAM per launch), then an even share of the leftover tiles' planes.
+//    Level-0 planes (the tile plus a (K-1)+1 halo ring) arrive by TMA
+//    (cp.async.bulk.tensor.3d) into a shared-memory ring guarded by
+//    mbarriers (planes t-2 .. t+STAGES-3 of step t, as deep as the shared
+//    memory left by the level buffers allows).
 //  * SMEM tier (locality enhancer): levels 1..K-1 are computed on the same
 //    region (overlapped tiling: the valid part shrinks by one cell per level)
 //    as a wavefront along a0 — level l works on plane t-2l — so K steps cost
@@ -43,7 +46,6 @@ namespace {
 constexpr int R1X = 64;  // level-1 region width  (a2)
 constexpr int VX = 2;    // columns per thread along a2
 constexpr int NLX = R1X / VX;  // 32 lanes
-constexpr int STAGES = 5;  // planes t-2 .. t+2 of the level-0 ring
 
 // Region height and column-stack depth: a warp owns VY rows of the R1Y-row
 // level-1 region, so a CTA has R1Y / VY warps.
@@ -54,7 +56,10 @@ struct Shape {
     static constexpr int NLY = R1Y / VY;    // warps
     static constexpr int NT = NLX * NLY;    // threads
     static constexpr int BY0 = R1Y + 2;     // TMA box height: 1 extra row per side
-    static constexpr int LEVY = R1Y + 2;    // level buffer rows (1 padding row per side)
+    // Level buffers keep only the rows other warps read: each warp's first
+    // and last row (warp w's at buffer rows 2w+1 and 2w+2), plus one padding
+    // row per side.  For VY = 2 that is every region row.
+    static constexpr int LEVY = 2 * NLY + 2;
 };
 // 512 threads, 2x2 columns per thread.  A 4x2 stack with 256 threads
 // (half the SMEM traffic per point, 186-239 registers) measured 2-4% slower
@@ -95,17 +100,33 @@ constexpr int lev_bytes() {
     return (G::LEVY * R1X * (int)sizeof(T) + 127) / 128 * 128;
 }
 constexpr int NLEV = 3;  // level-l planes are read two steps after they are written
+constexpr int kSmemMax = 227 * 1024;  // dynamic shared memory per CTA (sm_100)
+constexpr int kMaxStages = 10;
+// Ring depth: planes t-2 .. t+STAGES-3 of the level-0 ring, i.e. STAGES-2
+// planes in flight ahead of the one being consumed.  As deep as the shared
+// memory left by the level buffers allows: the persistent K >= 2 schedule
+// keeps one CTA per SM, so the planes in flight per SM bound the HBM rate
+// (measured: K = 2 and K = 3 both stalled near 4.6 TB/s with 3 in flight).
+template <typename T, int K, typename G>
+constexpr int stages() {
+    if (K == 1) return 5;  // chunked schedule, several CTAs per SM: HBM-bound already
+    const int avail = kSmemMax - NLEV * (K - 1) * lev_bytes<T, G>() - kMaxStages * 8;
+    const int n = avail / slot_bytes<T, G>();
+    return n < kMaxStages ? n : kMaxStages;
+}
 template <typename T, int K, typename G>
 constexpr int smem_bytes() {
-    return STAGES * slot_bytes<T, G>() + NLEV * (K - 1) * lev_bytes<T, G>() + STAGES * 8;
+    return stages<T, K, G>() * slot_bytes<T, G>() + NLEV * (K - 1) * lev_bytes<T, G>() +
+           kMaxStages * 8;
 }
 
 template <typename T>
 struct TbArgs {
     int n0, n1, n2;
     int tiles_x, tiles_y;
-    long long per_cta;  // (tile, plane) positions per CTA (persistent schedule), or
+    long long per_cta;  // remainder (tile, plane) positions per CTA (persistent), or
     int chunk;          // > 0: one chunk of a0 planes per CTA, tiles fastest
+    int full_tiles;     // persistent: whole tiles per CTA before the remainder
     int lo0, hi0;  // output planes [lo0, hi0) of a0
     int h0, h1, off2;
     long long pitch0, pitch1, origin;
@@ -153,11 +174,13 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                                           const bool (&cout)[G::VY][VX],
                                           T (&Hs)[K][3][G::VY][VX]) {
     constexpr int VY = G::VY;
+    constexpr int STAGES = stages<T, K, G>();
     using P2 = typename Pair<T>::type;
     constexpr int SLOT = slot_bytes<T, G>() / (int)sizeof(T);
     constexpr int LEV = lev_bytes<T, G>() / (int)sizeof(T);
     constexpr int BX = BX0<T>, PL = PADL<T>;
     const int t = t_begin + it;
+    const int ly2 = 2 * (y / VY);  // level-buffer row of this warp's first row, minus 1
     // ring position of plane t (slot and mbarrier phase), advanced by one per
     // step instead of divided out of the load count
     const int slot = rslot;
@@ -187,8 +210,9 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
             d = *reinterpret_cast<const P2*>(Pm + (y + VY + 1) * BX + x + PL);
         } else {
             const T* L = lev + ((l - 2) * NLEV + sC) * LEV;
-            u = *reinterpret_cast<const P2*>(L + (y) * R1X + x);
-            d = *reinterpret_cast<const P2*>(L + (y + VY + 1) * R1X + x);
+            // last row of the warp above, first row of the warp below
+            u = *reinterpret_cast<const P2*>(L + (ly2) * R1X + x);
+            d = *reinterpret_cast<const P2*>(L + (ly2 + 3) * R1X + x);
         }
         T res[VY][VX];
 #pragma unroll
@@ -236,7 +260,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                     P2 v;
                     v.x = res[cy][0];
                     v.y = res[cy][1];
-                    *reinterpret_cast<P2*>(L + (y + cy + 1) * R1X + x) = v;
+                    *reinterpret_cast<P2*>(L + (ly2 + (cy == 0 ? 1 : 2)) * R1X + x) = v;
                 }
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) Hs[l][sC][cy][cx] = res[cy][cx];
@@ -289,6 +313,8 @@ __global__ void __launch_bounds__(G::NT, 1)
                 const __grid_constant__ TbArgs<T> a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int VY = G::VY, R1Y = G::R1Y, BY0 = G::BY0;
+    constexpr int STAGES = stages<T, K, G>();
+    static_assert(STAGES >= 5, "the ring holds planes t-2 .. t+2 at least");
     constexpr int SLOT = slot_bytes<T, G>() / (int)sizeof(T);
     T* ring = reinterpret_cast<T*>(smem);
     T* lev = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T, G>());
@@ -310,24 +336,29 @@ __global__ void __launch_bounds__(G::NT, 1)
     }
     __syncthreads();
 
-    // Persistent schedule: the CTA owns positions [pos, end) of the
-    // (tile, plane) space, tile-major, and streams them as segments of
-    // consecutive planes of one tile; only a tile change refills the
-    // wavefront (3K steps), instead of every chunk of a one-chunk-per-CTA
-    // grid.
+    // Persistent schedule (K >= 2), in two phases.  Phase 1: CTA b streams
+    // whole tiles b, b + W, b + 2W, ... (W = grid size), all CTAs starting
+    // at the same plane, so tiles that are neighbours in (a1, a2) run
+    // side by side at the same a0 position and the halo rows their TMA
+    // boxes share are read from HBM once and from L2 the second time.
+    // Phase 2: the tiles left over (fewer than W) are one tile-major
+    // (tile, plane) position space split evenly over the CTAs.  Only a tile
+    // change refills the wavefront (3K steps).
     // K = 1 is HBM-bound: it keeps one chunk per CTA with the tiles of a
-    // chunk on consecutive CTAs, so neighbouring tiles read their shared
-    // halo rows at the same time and L2 serves the second read.
+    // chunk on consecutive CTAs (the same L2 sharing, many CTAs per SM).
     const long long span = a.hi0 - a.lo0;
-    const long long total = (long long)a.tiles_x * a.tiles_y * span;
+    const int ntile = a.tiles_x * a.tiles_y;
+    const int tile_rem0 = a.full_tiles * (int)gridDim.x;  // first phase-2 tile
+    const long long total = (long long)(ntile - tile_rem0) * span;
     long long pos, end;
+    int full_left = 0, full_tile = blockIdx.x;
     if (a.chunk > 0) {
-        const int ntile = a.tiles_x * a.tiles_y;
         const int tile = blockIdx.x % ntile, bz = blockIdx.x / ntile;
         const long long off = (long long)bz * a.chunk;
         pos = (long long)tile * span + off;
         end = pos + min((long long)a.chunk, span - off);
     } else {
+        full_left = a.full_tiles;
         pos = (long long)blockIdx.x * a.per_cta;
         end = min(pos + a.per_cta, total);
     }
@@ -344,11 +375,21 @@ __global__ void __launch_bounds__(G::NT, 1)
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) Hs[l][s][cy][cx] = T(0);
 
-    while (pos < end) {
-        const int tile = (int)(pos / span);
-        const int i0 = a.lo0 + (int)(pos - (long long)tile * span);
-        const int i1 = (int)min((long long)a.hi0, (long long)i0 + (end - pos));
-        pos += i1 - i0;
+    while (full_left > 0 || pos < end) {
+        int tile, i0, i1;
+        if (full_left > 0) {
+            tile = full_tile;
+            i0 = a.lo0;
+            i1 = a.hi0;
+            full_tile += gridDim.x;
+            --full_left;
+        } else {
+            const int t = (int)(pos / span);
+            i0 = a.lo0 + (int)(pos - (long long)t * span);
+            i1 = (int)min((long long)a.hi0, (long long)i0 + (end - pos));
+            pos += i1 - i0;
+            tile = (a.chunk > 0 ? 0 : tile_rem0) + t;
+        }
         const int bx = tile % a.tiles_x;
         const int by = tile / a.tiles_x;
         const int gx = bx * TX - HX;       // global a2 of region-1 column 0
@@ -501,15 +542,24 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     const int64_t span = a.hi0 - a.lo0;
     const long long total = tiles * span;
     unsigned grid;
+    a.full_tiles = 0;
     if (K == 1) {
         a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 2 * K, 48);
         a.per_cta = 0;
         grid = (unsigned)(tiles * ((span + a.chunk - 1) / a.chunk));
     } else {
-        const long long ctas = std::min<long long>((long long)nsm * per_sm, total);
+        const long long slots = (long long)nsm * per_sm;
         a.chunk = 0;
-        a.per_cta = (total + ctas - 1) / ctas;
-        grid = (unsigned)((total + a.per_cta - 1) / a.per_cta);
+        if (tiles >= slots) {  // phase 1: whole tiles, aligned planes
+            grid = (unsigned)slots;
+            a.full_tiles = (int)(tiles / slots);
+            const long long rest = (tiles - (long long)a.full_tiles * slots) * span;
+            a.per_cta = (rest + slots - 1) / slots;
+        } else {  // fewer tiles than SMs: the position space split evenly
+            const long long ctas = std::min<long long>(slots, total);
+            a.per_cta = (total + ctas - 1) / ctas;
+            grid = (unsigned)((total + a.per_cta - 1) / a.per_cta);
+        }
     }
     a.h0 = (int)g.h[0];
     a.h1 = (int)g.h[1];
@@ -533,13 +583,21 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     return Status::Ok();
 }
 
+// K = 3 uses 3x2 column stacks in a 64 x 36 region (384 threads, 168
+// registers, 60 x 32 output tiles): against 2x2 stacks in 64 x 32 (512
+// threads) it moves 22% fewer shared-memory / shuffle wavefronts per point
+// (the warp-edge rows are a third of the rows instead of all of them),
+// computes 5% fewer redundant cells per tile, and a 512^2 cross-section is
+// 144 whole tiles (one wave on 148 SMs).  Measured C3 FAST 689 -> 714 GS/s,
+// C5 772 -> 795.  K = 2 keeps 2x2 stacks (628 vs 515 GS/s).
+using ShapeC = Shape<3, 36>;
+
 template <typename T, bool EXACT>
 Status launch_m(const LaunchCtx& c, const void* in, void* out, int k) {
     switch (k) {
         case 1: return launch_k<T, 1, EXACT, ShapeA>(c, in, out);
         case 2: return launch_k<T, 2, EXACT, ShapeA>(c, in, out);
-        case 3:
-            return launch_k<T, 3, EXACT, ShapeA, true>(c, in, out);
+        case 3: return launch_k<T, 3, EXACT, ShapeC, true>(c, in, out);
         default: return Status::Err(TSR_EUNSUPPORTED, "tb3d: fused steps must be 1..3");
     }
 }
