@@ -241,7 +241,9 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
         // (only the SEL instantiations: 1 = boundary columns/rows of this
         // warp on interior planes, 2 = also a0-boundary planes / wavefront
         // fill and drain).
-        if constexpr (SEL != 0) {
+        // Level K's values are only stored where cout (interior) holds, so
+        // it needs no select.
+        if (SEL != 0 && l < K) {
             const bool pint = SEL == 1 || (p >= 0 && p < a.n0);
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy)
@@ -555,6 +557,13 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
             a.full_tiles = (int)(tiles / slots);
             const long long rest = (tiles - (long long)a.full_tiles * slots) * span;
             a.per_cta = (rest + slots - 1) / slots;
+        } else if (tiles * 10 >= slots * 9) {
+            // nearly one tile per SM (C3: 144 tiles, 148 SMs): one whole tile
+            // per CTA keeps the planes aligned; an even split would leave 4
+            // SMs less idle but put neighbouring tiles at different planes
+            grid = (unsigned)tiles;
+            a.full_tiles = 1;
+            a.per_cta = 0;
         } else {  // fewer tiles than SMs: the position space split evenly
             const long long ctas = std::min<long long>(slots, total);
             a.per_cta = (total + ctas - 1) / ctas;
