@@ -171,7 +171,7 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
                                           int t_begin,
                                           int i0, int i1, int lx, int x, int y, long long& ooff,
                                           const bool (&cint)[G::VY][VX],
-                                          const bool (&cout)[G::VY][VX],
+                                          const bool (&cout)[G::VY][VX], bool hl,
                                           T (&Hs)[K][3][G::VY][VX]) {
     constexpr int VY = G::VY;
     constexpr int STAGES = stages<T, K, G>();
@@ -243,7 +243,15 @@ __device__ __forceinline__ void tb3d_step(const TbArgs<T>& a, T* __restrict__ ou
         // fill and drain).
         // Level K's values are only stored where cout (interior) holds, so
         // it needs no select.
-        if (SEL != 0 && l < K) {
+        if ((SEL == 3 || SEL == 4) && l < K) {
+            // a2-edge warp whose rows are all interior: the one non-interior
+            // cell an interior cell reads is the halo column, held by lane
+            // `hl` in column 1 (SEL 3) or 0 (SEL 4); cells beyond it feed only it
+            constexpr int hc = SEL == 3 ? 1 : 0;
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+                if (hl) res[cy][hc] = Hs[l - 1][sC][cy][hc];
+        } else if (SEL != 0 && l < K) {
             const bool pint = SEL == 1 || (p >= 0 && p < a.n0);
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy)
@@ -455,6 +463,21 @@ __global__ void __launch_bounds__(G::NT, 1)
 #pragma unroll
             for (int cx = 0; cx < VX; ++cx) mine &= cint[cy][cx];
         const bool warp_int = __all_sync(0xffffffffu, mine);  // no boundary column in this warp
+        // a2-edge warps with every row interior (the bulk of the boundary
+        // tiles): only the halo column next to the interior (a2 = -1 or n2)
+        // must keep its level-0 value; it sits in the same column slot of
+        // every such lane (region columns start 16-B aligned), so a
+        // one-column select tier serves them
+        bool rows_in = true, hl0 = false, hl1 = false;
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy) rows_in &= gy + y + cy >= 0 && gy + y + cy < a.n1;
+        hl0 = gx + x == -1 || gx + x == a.n2;
+        hl1 = gx + x + 1 == -1 || gx + x + 1 == a.n2;
+        const bool warp_rows = __all_sync(0xffffffffu, rows_in);
+        const bool any0 = __any_sync(0xffffffffu, hl0), any1 = __any_sync(0xffffffffu, hl1);
+        const int edge_tier = warp_int || !warp_rows ? 0 : (any1 && !any0) ? 3
+                                                         : (any0 && !any1) ? 4 : 0;
+        const bool hl = edge_tier == 3 ? hl1 : hl0;
         // A unit of three steps runs select-free when the planes its levels
         // read (t-2K .. t-2) are interior, no column of this warp is on the
         // a1/a2 boundary and every plane level K produces is one of this
@@ -467,7 +490,7 @@ __global__ void __launch_bounds__(G::NT, 1)
         };
 #define TB3D_STEP(PH, IT, SEL)                                                                  \
     tb3d_step<T, K, EXACT, PH, SEL, G, EARLY0, MIRROR>(a, out, ring, lev, bar, rslot, rphase, IT, t_begin, i0, i1, \
-                                               lx, x, y, ooff, cint, cout, Hs);                 \
+                                               lx, x, y, ooff, cint, cout, hl, Hs);             \
     after(IT);
         // The clear units form one interval of `it` (every condition of
         // clear() is an interval), so the tier is chosen once per segment:
@@ -492,6 +515,18 @@ __global__ void __launch_bounds__(G::NT, 1)
                 TB3D_STEP(0, it, 0)
                 TB3D_STEP(1, it + 1, 0)
                 TB3D_STEP(2, it + 2, 0)
+            }
+        } else if (!MIRROR && edge_tier == 3) {
+            for (; it < niter && unit_clear(it); it += 3) {
+                TB3D_STEP(0, it, 3)
+                TB3D_STEP(1, it + 1, 3)
+                TB3D_STEP(2, it + 2, 3)
+            }
+        } else if (!MIRROR && edge_tier == 4) {
+            for (; it < niter && unit_clear(it); it += 3) {
+                TB3D_STEP(0, it, 4)
+                TB3D_STEP(1, it + 1, 4)
+                TB3D_STEP(2, it + 2, 4)
             }
         } else if (!MIRROR) {  // a2/a1-edge warps of boundary tiles on interior planes
                                // (the seam-pass instance keeps two tiers: a third spills it)
