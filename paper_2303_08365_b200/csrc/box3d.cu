@@ -84,6 +84,31 @@ struct VecT<double, 2> {
     using type = double2;
 };
 
+// One row of a thread's (VX + 2)-wide neighbourhood: its VX cells by vector
+// loads, the two outer cells from the neighbouring lanes by shuffle (W lanes
+// span one row of the region), and only the row's first / last lane takes
+// the region edge cell from shared memory — a broadcast load every lane
+// issues (one address per row), so no 16-B-strided scalar loads and no bank
+// conflicts.  `row` points at the thread's first cell, x its region column.
+template <typename T, int W>
+__device__ __forceinline__ void load_row(const T* row, int x, int lx, T (&nbr)[VX + 2]) {
+    using V4 = typename VecT<T, 16 / sizeof(T)>::type;
+    constexpr int NV = 16 / sizeof(T);
+#pragma unroll
+    for (int v = 0; v < VX; v += NV) {
+        const V4 vv = *reinterpret_cast<const V4*>(row + v);
+        const T* e = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+        for (int u = 0; u < NV; ++u) nbr[1 + v + u] = e[u];
+    }
+    const T left = __shfl_up_sync(0xffffffffu, nbr[VX], 1, W);
+    const T right = __shfl_down_sync(0xffffffffu, nbr[1], 1, W);
+    const T* row0 = row - x;  // region column 0 of this row
+    const T el = row0[-1], er = row0[W * VX];
+    nbr[0] = lx == 0 ? el : left;
+    nbr[VX + 1] = lx == W - 1 ? er : right;
+}
+
 // Nine taps of one plane offset applied to the neighbourhood nb (rows y-1..y+VY,
 // cols x-1..x+VX) for every output of the thread's 4x4 tile.
 // Q: nb holds q = w*v (uniform-weight kernel, see stream2d.cu): every tap is
@@ -110,12 +135,43 @@ __device__ __forceinline__ void apply9(const T* __restrict__ w, const T (&nb)[VY
         }
 }
 
-// MODE: 0 FAST, 1 EXACT, 2 Q (uniform weights: shared products, exact)
+// SEP (FAST mode, uniform weights): the 27-point box sum factorises into
+// row sums along a2, then column sums along a1 (this function: the 2-D
+// 9-point sum of one plane for every output of the thread's 4x4 tile, 5
+// adds per output with the shared pair sums), then the three plane sums
+// along a0, times the one weight: 8 operations per output instead of 27
+// (Q) or 27 FMAs (FAST), within the 1e-5 fp32 / 1e-12 fp64 tolerance of the
+// oracle's order (only the rounding of the reassociated sum differs).
+template <typename T>
+__device__ __forceinline__ void plane_sum9(const T (&nb)[VY + 2][VX + 2], T (&s)[VY][VX]) {
+    static_assert(VX == 4, "pair sums assume four outputs per row");
+    T r[VY + 2][VX];
+#pragma unroll
+    for (int q = 0; q < VY + 2; ++q) {
+        const T p0 = nb[q][1] + nb[q][2], p2 = nb[q][3] + nb[q][4];
+        r[q][0] = nb[q][0] + p0;
+        r[q][1] = p0 + nb[q][3];
+        r[q][2] = nb[q][2] + p2;
+        r[q][3] = p2 + nb[q][5];
+    }
+#pragma unroll
+    for (int cx = 0; cx < VX; ++cx) {
+#pragma unroll
+        for (int cy = 0; cy < VY; cy += 2) {
+            const T m = r[cy + 1][cx] + r[cy + 2][cx];  // shared by rows cy and cy+1
+            s[cy][cx] = r[cy][cx] + m;
+            s[cy + 1][cx] = m + r[cy + 3][cx];
+        }
+    }
+}
+
+// MODE: 0 FAST, 1 EXACT, 2 Q (uniform weights: shared products, exact),
+// 3 SEP (uniform weights, FAST: separable sums)
 template <typename T, int MODE>
 __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
                                                    const __grid_constant__ CUtensorMap tmap,
                                                    const __grid_constant__ BoxArgs<T> a) {
-    constexpr bool EXACT = MODE != 0, Q = MODE == 2;
+    constexpr bool EXACT = MODE == 1 || MODE == 2, Q = MODE == 2, SEP = MODE == 3;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int SLOT = slot1_bytes<T>() / (int)sizeof(T);
     constexpr int BX = BXW1<T>, PL = PAD<T>;
@@ -174,6 +230,8 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
         const int slot = it % STAGES;
         mbar_wait(&bar[slot], (it / STAGES) & 1);
         const T* P = ring + slot * SLOT;
+        // (direct edge loads here: the shuffled rows of load_row measured 4%
+        // slower in this single-level, HBM-bound kernel)
         T nb[VY + 2][VX + 2];
 #pragma unroll
         for (int r = 0; r < VY + 2; ++r) {
@@ -201,8 +259,17 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
             tma_load_3d(ring + slot * SLOT, &tmap, &bar[slot], c0, c1,
                         a.h0 + t_begin + it + STAGES);
         }
-        // finish output q-1 (di = +1 taps)
-        apply9<EXACT, false, T, Q>(a.w + 18, nb, accB);
+        T ps[VY][VX];  // SEP: this plane's 9-point sums
+        if constexpr (SEP) {
+            plane_sum9(nb, ps);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) accB[cy][cx] = a.w[0] * (accB[cy][cx] + ps[cy][cx]);
+        } else {
+            // finish output q-1 (di = +1 taps)
+            apply9<EXACT, false, T, Q>(a.w + 18, nb, accB);
+        }
         const int po = q - 1;
         if (it >= 2 && po < i1) {
             T* o = orow;  // plane po
@@ -215,12 +282,22 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
         }
         orow += a.pitch0;
         // output q continues (di = 0), output q+1 starts (di = -1)
-        apply9<EXACT, false, T, Q>(a.w + 9, nb, accA);
+        if constexpr (SEP) {
 #pragma unroll
-        for (int cy = 0; cy < VY; ++cy)
+            for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-            for (int cx = 0; cx < VX; ++cx) accB[cy][cx] = accA[cy][cx];
-        apply9<EXACT, true, T, Q>(a.w, nb, accA);
+                for (int cx = 0; cx < VX; ++cx) {
+                    accB[cy][cx] = accA[cy][cx] + ps[cy][cx];
+                    accA[cy][cx] = ps[cy][cx];
+                }
+        } else {
+            apply9<EXACT, false, T, Q>(a.w + 9, nb, accA);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) accB[cy][cx] = accA[cy][cx];
+            apply9<EXACT, true, T, Q>(a.w, nb, accA);
+        }
     }
 }
 
@@ -258,7 +335,7 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
                                                       const __grid_constant__ CUtensorMap tmap,
                                                       const __grid_constant__ BoxArgs<T> a) {
-    constexpr bool EXACT = MODE != 0, Q = MODE == 2;
+    constexpr bool EXACT = MODE == 1 || MODE == 2, Q = MODE == 2, SEP = MODE == 3;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
     constexpr int BE = b_bytes<T>() / (int)sizeof(T);
@@ -326,18 +403,7 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
     constexpr int NV = 16 / sizeof(T);
     auto read_nb = [&](const T* rowbase, int pitch, T(&nb)[VY + 2][VX + 2]) {
 #pragma unroll
-        for (int r = 0; r < VY + 2; ++r) {
-            const T* row = rowbase + (y + r) * pitch;
-            nb[r][0] = row[-1];
-#pragma unroll
-            for (int v = 0; v < VX; v += NV) {
-                const V4 vv = *reinterpret_cast<const V4*>(row + v);
-                const T* e = reinterpret_cast<const T*>(&vv);
-#pragma unroll
-                for (int u = 0; u < NV; ++u) nb[r][1 + v + u] = e[u];
-            }
-            nb[r][VX + 1] = row[VX];
-        }
+        for (int r = 0; r < VY + 2; ++r) load_row<T, NLX>(rowbase + (y + r) * pitch, x, lx, nb[r]);
     };
 
     for (int it = 0; it < niter; ++it) {
@@ -354,23 +420,49 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
                 for (int c = 0; c < VX + 2; ++c) nb[r][c] = mul_rn(a.w[0], nb[r][c]);
         }
         // level 1: finish q-1, continue q, start q+1
-        apply9<EXACT, false, T, Q>(a.w + 18, nb, a1B);
+        T ps[VY][VX];
+        if constexpr (SEP) {
+            plane_sum9(nb, ps);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) a1B[cy][cx] = a.w[0] * (a1B[cy][cx] + ps[cy][cx]);
+        } else {
+            apply9<EXACT, false, T, Q>(a.w + 18, nb, a1B);
+        }
         T l1[VY][VX];
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-            for (int cx = 0; cx < VX; ++cx) {
-                l1[cy][cx] = Q ? mul_rn(a.w[0], a1B[cy][cx]) : a1B[cy][cx];
-                if (sel && !(cint[cy][cx] && q - 1 >= 0 && q - 1 < a.n0))
-                    l1[cy][cx] = keep0[cy][cx];
-                keep0[cy][cx] = nb[cy + 1][cx + 1];
-            }
-        apply9<EXACT, false, T, Q>(a.w + 9, nb, a1A);
+            for (int cx = 0; cx < VX; ++cx) l1[cy][cx] = Q ? mul_rn(a.w[0], a1B[cy][cx]) : a1B[cy][cx];
+        if (sel) {  // warp-uniform: boundary warps and a0-boundary planes only
+            const bool pint = q - 1 >= 0 && q - 1 < a.n0;
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx)
+                    if (!(pint && cint[cy][cx])) l1[cy][cx] = keep0[cy][cx];
+        }
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-            for (int cx = 0; cx < VX; ++cx) a1B[cy][cx] = a1A[cy][cx];
-        apply9<EXACT, true, T, Q>(a.w, nb, a1A);
+            for (int cx = 0; cx < VX; ++cx) keep0[cy][cx] = nb[cy + 1][cx + 1];
+        if constexpr (SEP) {
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) {
+                    a1B[cy][cx] = a1A[cy][cx] + ps[cy][cx];
+                    a1A[cy][cx] = ps[cy][cx];
+                }
+        } else {
+            apply9<EXACT, false, T, Q>(a.w + 9, nb, a1A);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) a1B[cy][cx] = a1A[cy][cx];
+            apply9<EXACT, true, T, Q>(a.w, nb, a1A);
+        }
         // publish level-1 plane q-1: cell (y, x) at row y+1, column x+PAD
         T* B = buf + (((q - 1) % NB + NB) % NB) * BE;
 #pragma unroll
@@ -394,7 +486,16 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
         // level 2 on level-1 plane q-1: finish q-2, continue q-1, start q
         T nb2[VY + 2][VX + 2];
         read_nb(B + PL + x, BW, nb2);  // buffer rows y..y+VY+1 = region rows y-1..y+VY
-        apply9<EXACT, false, T, Q>(a.w + 18, nb2, a2B);
+        T ps2[VY][VX];
+        if constexpr (SEP) {
+            plane_sum9(nb2, ps2);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) a2B[cy][cx] = a.w[0] * (a2B[cy][cx] + ps2[cy][cx]);
+        } else {
+            apply9<EXACT, false, T, Q>(a.w + 18, nb2, a2B);
+        }
         const int po = q - 2;
         if (it >= 4 && po < i1) {
             // stored cells are interior (cout implies cint): no Dirichlet select
@@ -409,12 +510,22 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
                 if (a.mirror) store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, v, cout[cy]);
             }
         }
-        apply9<EXACT, false, T, Q>(a.w + 9, nb2, a2A);
+        if constexpr (SEP) {
 #pragma unroll
-        for (int cy = 0; cy < VY; ++cy)
+            for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-            for (int cx = 0; cx < VX; ++cx) a2B[cy][cx] = a2A[cy][cx];
-        apply9<EXACT, true, T, Q>(a.w, nb2, a2A);
+                for (int cx = 0; cx < VX; ++cx) {
+                    a2B[cy][cx] = a2A[cy][cx] + ps2[cy][cx];
+                    a2A[cy][cx] = ps2[cy][cx];
+                }
+        } else {
+            apply9<EXACT, false, T, Q>(a.w + 9, nb2, a2A);
+#pragma unroll
+            for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < VX; ++cx) a2B[cy][cx] = a2A[cy][cx];
+            apply9<EXACT, true, T, Q>(a.w, nb2, a2A);
+        }
     }
 }
 
@@ -422,9 +533,13 @@ bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused)
     if (t.dims != 3 || t.shape != TSR_BOX || t.radius != 1 || t.ntaps != 27) return false;
     if (g.n[0] + 2 * g.h[0] > (1 << 30) || g.n[1] + 2 * g.h[1] > (1 << 30)) return false;
     *max_fused = 2;
-    *default_fused = 1;  // k=2 is FMA-issue-bound at the same rate
+    *default_fused = 1;  // EXACT: k=2 is FP-issue-bound at the same rate
     return true;
 }
+
+// FAST with uniform weights runs the separable sums (8 operations per
+// update): k = 2 halves the HBM traffic per step (C4: 714 -> 799 GS/s).
+int fast_default(const TapSet& t) { return uniform_weights(t) ? 2 : 1; }
 
 template <typename T, int MODE>
 Status launch(const LaunchCtx& c, const void* in, void* out) {
@@ -504,14 +619,23 @@ Status launch2(const LaunchCtx& c, const void* in, void* out) {
 
 template <typename T>
 Status run_t(const LaunchCtx& c, const void* in, void* out, int k) {
-    const int mode = uniform_weights(*c.taps) ? 2 : c.exact ? 1 : 0;  // Q serves both modes
+    // uniform weights: Q in EXACT mode (bitwise), separable sums in FAST
+    const int mode = uniform_weights(*c.taps) ? (c.exact ? 2 : 3) : c.exact ? 1 : 0;
     if (k == 2) {
-        if (mode == 2) return launch2<T, 2>(c, in, out);
-        return mode ? launch2<T, 1>(c, in, out) : launch2<T, 0>(c, in, out);
+        switch (mode) {
+            case 0: return launch2<T, 0>(c, in, out);
+            case 1: return launch2<T, 1>(c, in, out);
+            case 2: return launch2<T, 2>(c, in, out);
+            default: return launch2<T, 3>(c, in, out);
+        }
     }
     if (k != 1) return Status::Err(TSR_EUNSUPPORTED, "box3d fuses one or two steps per pass");
-    if (mode == 2) return launch<T, 2>(c, in, out);
-    return mode ? launch<T, 1>(c, in, out) : launch<T, 0>(c, in, out);
+    switch (mode) {
+        case 0: return launch<T, 0>(c, in, out);
+        case 1: return launch<T, 1>(c, in, out);
+        case 2: return launch<T, 2>(c, in, out);
+        default: return launch<T, 3>(c, in, out);
+    }
 }
 
 Status run(const LaunchCtx& c, const void* in, void* out, int k) {
@@ -521,6 +645,6 @@ Status run(const LaunchCtx& c, const void* in, void* out, int k) {
 
 }  // namespace
 
-extern const Engine kBox3dEngine = {"box3d_r1_planesum", supports, run};
+extern const Engine kBox3dEngine = {"box3d_r1_planesum", supports, run, fast_default};
 
 }  // namespace tsr

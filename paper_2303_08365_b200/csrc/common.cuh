@@ -208,6 +208,9 @@ struct Engine {
     const char* name;
     bool (*supports)(const Geo&, const TapSet&, int* max_fused, int* default_fused);
     Status (*run)(const LaunchCtx&, const void* in, void* out, int k);
+    // Optional: the default fused depth in FAST mode when it differs from
+    // the EXACT one (nullptr = same as supports()'s default_fused).
+    int (*fast_default)(const TapSet&) = nullptr;
 };
 const Engine* find_engine(const Geo& g, const TapSet& t, int* max_fused, int* default_fused);
 

@@ -454,11 +454,13 @@ def test_reduced_shape_full_steps(ts, orc, cfg):
     st = ts.run_gpu(got, k, steps, fused_steps=fused, mode="exact")
     assert st.fused_steps == fused
     assert both_buffers_equal(got, ref)
-    if cfg == "c4":
-        fast = a.copy()
-        ts.run_gpu(fast, k, steps, fused_steps=fused, mode="fast")
-        d = ts.deviation(fast, ref)
-        assert d["max_rel_deviation"] <= TOL["f32"] and d["l2_rel_err"] <= TOL["f32"]
+    if cfg == "c4":  # FAST = separable box sums (uniform weights), one and two levels
+        for kf in (1, 2):
+            fast = a.copy()
+            st = ts.run_gpu(fast, k, steps, fused_steps=kf, mode="fast")
+            assert st.fused_steps == kf
+            d = ts.deviation(fast, ref)
+            assert d["max_rel_deviation"] <= TOL["f32"] and d["l2_rel_err"] <= TOL["f32"], (kf, d)
 
 
 def test_staged_transfers_halo_and_cache_sizes(ts, orc):
