@@ -283,3 +283,21 @@ class Reference:
             elif tok[0] == "final":
                 res["final_center"] = float.fromhex(tok[1])
         return res
+
+    def plan_tiles(self, extent, tile, tb: int, radius: int):
+        """The reference's plan_tiles + count_coverage: (upright, inverted,
+        (all_ones, min, max), [(kind tuple, index tuple, wave), ...])."""
+        d = len(extent)
+        ext = (ctypes.c_int64 * 3)(*(list(extent) + [1] * (3 - d)))
+        til = (ctypes.c_int64 * 3)(*(list(tile) + [1] * (3 - d)))
+        out = (ctypes.c_int64 * 5)()
+        cap = 1
+        for e, t in zip(extent, tile):
+            cap *= 2 * max(1, e // t)
+        tl = (ctypes.c_int32 * (7 * cap))()
+        self._err(self.L.ref_plan_tiles(d, ext, til, tb, radius, out, tl, ctypes.c_int64(cap)))
+        n = out[0] + out[1]
+        kinds = ("upright", "inverted")
+        tiles = [(tuple(kinds[tl[7 * i + a]] for a in range(d)),
+                  tuple(tl[7 * i + 3 + a] for a in range(d)), tl[7 * i + 6]) for i in range(n)]
+        return out[0], out[1], (bool(out[2]), out[3], out[4]), tiles

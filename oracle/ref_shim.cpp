@@ -272,4 +272,35 @@ int ref_dump_grid(const char* path, int dims, const int64_t* ext, const int64_t*
     }
 }
 
+// plan_tiles + count_coverage (tiling.cpp:48-135): out5 = {phase_a size,
+// phase_b size, all_ones, min_count, max_count}; tiles_out (capacity cap
+// tiles, 7 ints each: kind[3], index[3], wave) lists phase A then phase B.
+int ref_plan_tiles(int dims, const int64_t* ext, const int64_t* tile, int tb, int radius,
+                   int64_t* out5, int32_t* tiles_out, int64_t cap) {
+    try {
+        std::vector<Index> e(ext, ext + dims), t(tile, tile + dims);
+        const TilePlan p = plan_tiles(e, t, tb, radius);
+        const CoverageCount c = count_coverage(p);
+        out5[0] = static_cast<int64_t>(p.phase_a.size());
+        out5[1] = static_cast<int64_t>(p.phase_b.size());
+        out5[2] = c.all_ones();
+        out5[3] = c.min_count();
+        out5[4] = c.max_count();
+        int64_t n = 0;
+        for (const auto* ph : {&p.phase_a, &p.phase_b})
+            for (const Tile& x : *ph) {
+                if (n >= cap) break;
+                for (int a = 0; a < 3; ++a) {
+                    tiles_out[7 * n + a] = static_cast<int32_t>(x.kind[a]);
+                    tiles_out[7 * n + 3 + a] = static_cast<int32_t>(x.index[a]);
+                }
+                tiles_out[7 * n + 6] = x.wave;
+                ++n;
+            }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 }  // extern "C"

@@ -11,8 +11,8 @@ from .kernel import (StencilKernel, BenchmarkSpec, benchmark_names, benchmark_ta
                      box_kernel, find_benchmark, heat_coefficients, lattice_offsets, make_kernel,
                      star_kernel)
 from .grid import (BasicGrid, Grid, GridF, dump_grid, fill_random, grid_from_numpy, load_grid)
-from .run import (GpuStats, TilePlan, naive_run, naive_step, plan_tiles, release_cache,
-                  run_gpu, run_tessellated)
+from .run import (GpuStats, Tile, TilePlan, axis_range, count_coverage, naive_run, naive_step,
+                  plan_tiles, release_cache, run_gpu, run_tessellated, tile_range)
 from .metrics import RateReport, deviation, max_abs, max_rel_deviation, stencils_per_second
 from .device import DeviceGrid, layout_of
 from .harness import csv_header, csv_row, run_all, run_benchmark, write_csv
@@ -27,7 +27,7 @@ __all__ = [
     "StencilKernel", "BenchmarkSpec", "benchmark_names", "benchmark_table", "box_kernel",
     "find_benchmark", "heat_coefficients", "lattice_offsets", "make_kernel", "star_kernel",
     "BasicGrid", "Grid", "GridF", "dump_grid", "fill_random", "grid_from_numpy", "load_grid",
-    "GpuStats", "TilePlan", "naive_run", "naive_step", "plan_tiles", "release_cache", "run_gpu",
+    "GpuStats", "Tile", "TilePlan", "axis_range", "count_coverage", "tile_range", "naive_run", "naive_step", "plan_tiles", "release_cache", "run_gpu",
     "run_tessellated", "RateReport", "deviation", "max_abs", "max_rel_deviation",
     "stencils_per_second", "DeviceGrid", "layout_of", "run_benchmark", "run_all", "csv_header",
     "csv_row", "write_csv", "CommCostModel", "CommLog", "CommRecord", "PartitionPlan",

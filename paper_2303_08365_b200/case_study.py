@@ -70,6 +70,7 @@ class CaseStudyConfig:
     sample_every: int = 25
     fused_steps: int = 0      # 0 = engine default
     mode: str = "exact"
+    snapshot_every: int = 0   # > 0: TTRS snapshots of both fields every N steps (out_dir)
 
 
 def apply_full_scale(cfg: CaseStudyConfig) -> None:
@@ -147,9 +148,22 @@ def _init(grid, cfg: CaseStudyConfig, sigma: float) -> None:
                                          float(sigma)))
 
 
-def case_study_heat(cfg: CaseStudyConfig, out_dir: str | None = None, device=None) -> dict:
+def _snapshot_paths(out_dir: str, step: int):
+    return (os.path.join(out_dir, f"snapshot_{step}_fp64.ttrs"),
+            os.path.join(out_dir, f"snapshot_{step}_fp32.ttrs"))
+
+
+def case_study_heat(cfg: CaseStudyConfig, out_dir: str | None = None, device=None,
+                    resume_step: int | None = None) -> dict:
     """Runs the study; writes center_series.csv, error_table.csv,
-    metadata.txt and final.ttrs into `out_dir` when given."""
+    metadata.txt and final.ttrs into `out_dir` when given.
+
+    Long runs (the paper's 3.8e6 steps) checkpoint with
+    ``cfg.snapshot_every``: both device fields go to out_dir as TTRS dumps
+    (snapshot_<step>_fp64.ttrs / _fp32.ttrs, the reference's grid_io format)
+    without leaving HBM; ``resume_step`` restarts from those files and
+    produces the rest of the series, tables and artifacts exactly as the
+    uninterrupted run does."""
     import torch
     if cfg.extent < 16:
         raise ValueError("plate extent too small")
@@ -168,18 +182,29 @@ def case_study_heat(cfg: CaseStudyConfig, out_dir: str | None = None, device=Non
     _init(fp64, cfg, sigma)
     _init(fp32, cfg, sigma)
     dev = torch.device(device if device is not None else "cuda")
-    d64 = DeviceGrid(fp64, dev)
-    d32 = DeviceGrid(fp32, dev)
+    if resume_step is not None:
+        if out_dir is None or cfg.snapshot_every <= 0 or resume_step % cfg.snapshot_every:
+            raise ValueError("resume needs out_dir and a step on the snapshot stride")
+        if resume_step % cfg.sample_every or resume_step > cfg.steps:
+            raise ValueError("resume step must fall on the sampling stride")
+        p64, p32 = _snapshot_paths(out_dir, resume_step)
+        d64 = DeviceGrid.resume(p64, dev, "f64")
+        d32 = DeviceGrid.resume(p32, dev, "f32")
+    else:
+        d64 = DeviceGrid(fp64, dev)
+        d32 = DeviceGrid(fp32, dev)
     center = n // 2
 
     def center_of(dg: DeviceGrid) -> float:
         e = dg.layout.origin + center * dg.layout.pitch[0] + center
         return float(dg.buf[dg.cur][e].item())
 
-    res = {"series_steps": [0], "center_series": [float(fp64.at(center, center))],
+    done = 0 if resume_step is None else int(resume_step)
+    res = {"series_steps": [done],
+           "center_series": [float(fp64.at(center, center)) if resume_step is None
+                             else center_of(d64)],
            "checkpoint_steps": [], "checkpoint_errors": [], "artifacts": []}
     t64 = t32 = 0.0
-    done = 0
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     while done < cfg.steps:
         chunk = min(cfg.sample_every, cfg.steps - done)
@@ -193,6 +218,12 @@ def case_study_heat(cfg: CaseStudyConfig, out_dir: str | None = None, device=Non
         res["center_series"].append(center_of(d64))  # synchronises
         t64 += ev[0].elapsed_time(ev[1]) / 1e3
         t32 += ev[1].elapsed_time(ev[2]) / 1e3
+        if out_dir and cfg.snapshot_every > 0 and done % cfg.snapshot_every == 0:
+            os.makedirs(out_dir, exist_ok=True)
+            p64, p32 = _snapshot_paths(out_dir, done)
+            d64.snapshot(p64)
+            d32.snapshot(p32)
+            res["artifacts"] += [p64, p32]
         if done in cfg.checkpoints:
             h64, h32 = Grid([n, n], [1, 1]), GridF([n, n], [1, 1])
             _init(h64, cfg, sigma)
@@ -204,7 +235,7 @@ def case_study_heat(cfg: CaseStudyConfig, out_dir: str | None = None, device=Non
             res["checkpoint_errors"].append(compare_precision(h64, h32))
             fp64, fp32 = h64, h32
     res["final_center"] = res["center_series"][-1]
-    pts = n * n * cfg.steps
+    pts = n * n * (cfg.steps - (resume_step or 0))
     res["fp64_device_s"] = t64
     res["fp32_device_s"] = t32
     res["fp64_gstencil_s"] = pts / t64 / 1e9 if t64 > 0 else 0.0

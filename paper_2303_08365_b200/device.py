@@ -154,3 +154,43 @@ class DeviceGrid:
             (stream if stream is not None
              else self.torch.cuda.current_stream(self.device)).synchronize()
         self.steps_done = 0
+
+    # ---- TTRS snapshot / resume (proj/src/grid_io.cpp:34-68) -------------
+    def snapshot(self, path: str, stream=None) -> None:
+        """Writes the current device state (interior and halo of the
+        current buffer) as a TTRS grid dump, the reference's format
+        (dump_grid, grid_io.cpp:34-45: fp64 payload; an fp32 grid is
+        widened, which is exact).  The device state is untouched, so a long
+        run can checkpoint every N steps and keep going."""
+        from .grid import Grid, GridF, dump_grid
+        cls = Grid if self.esize == 8 else GridF
+        host = cls(list(self.extent), list(self.halo))
+        L = _abi.lib()
+        s = self._stream(stream)
+        with self.torch.cuda.device(self.device):
+            _abi.check(L.tsr_download(ctypes.byref(self.desc), ctypes.byref(self.layout),
+                                      self.ptr(self.cur), host.c_buffers()[0], 0, s))
+            (stream if stream is not None
+             else self.torch.cuda.current_stream(self.device)).synchronize()
+        if self.esize == 4:
+            wide = Grid(list(self.extent), list(self.halo))
+            wide.buffer(0)[:] = host.buffer(0).astype("f8")
+            host = wide
+        dump_grid(path, host)
+
+    @classmethod
+    def resume(cls, path: str, device=None, dtype: str = "f64") -> "DeviceGrid":
+        """A DeviceGrid holding a TTRS dump (load_grid, grid_io.cpp:47-68)
+        as its current state; dtype "f32" narrows the payload (exact for a
+        dump written from an fp32 grid)."""
+        from .grid import GridF, load_grid
+        g = load_grid(path)
+        if dtype == "f32":
+            f = GridF(list(g.extent), list(g.halo))
+            for w in (0, 1):
+                f.buffer(w)[:] = g.buffer(w).astype("f4")
+            g = f
+        elif dtype != "f64":
+            raise ValueError(f"unknown dtype {dtype!r}")
+        return cls(g, device)
+

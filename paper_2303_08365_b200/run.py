@@ -78,10 +78,26 @@ def naive_run(grid: BasicGrid, kernel: StencilKernel, steps: int) -> None:
     run_gpu(grid, kernel, steps)
 
 
+UPRIGHT, INVERTED = "upright", "inverted"  # PieceKind (tiling.hpp:16)
+
+
+@dataclass
+class Tile:
+    """tiling.hpp:18-23: per-axis piece kind, segment / anchor index and
+    anchor position; wave = number of inverted axes (0 = phase A)."""
+    kind: tuple
+    index: tuple
+    anchor: tuple
+    wave: int
+
+
 class TilePlan:
     """Two-phase tessellation plan (tiling.hpp:30-41).  On the GPU only `tb`
-    matters (the fused step count); extents and radius are validated like the
-    reference so a plan/grid mismatch raises the same errors."""
+    matters (the fused step count): the engine streams overlapped tiles
+    instead.  The plan itself is built exactly as the reference builds it
+    (validation, segment counts, phase A / phase B tile lists ordered by
+    wave), so ``upright_tiles`` / ``inverted_tiles`` / ``count_coverage``
+    answer as the reference's binding does (module.cpp:180-193)."""
 
     def __init__(self, extent, tile, tb, radius, segments):
         self.dims = len(extent)
@@ -90,24 +106,65 @@ class TilePlan:
         self.tb = int(tb)
         self.radius = int(radius)
         self.segments = list(segments)
+        self.phase_a, self.phase_b = [], []
+        # every (kind, index) product over the axes, kinds upright-first
+        # (tiling.cpp:80-100); phase B stable-sorted by wave
+        combos = [((), ())]
+        for a in range(self.dims):
+            combos = [(k + (kind,), i + (n,)) for k, i in combos
+                      for kind in (UPRIGHT, INVERTED) for n in range(self.segments[a])]
+        for kind, index in combos:
+            wave = sum(1 for k in kind if k == INVERTED)
+            t = Tile(kind, index, tuple(i * w for i, w in zip(index, self.tile)), wave)
+            (self.phase_a if wave == 0 else self.phase_b).append(t)
+        self.phase_b.sort(key=lambda t: t.wave)
 
     @property
     def upright_tiles(self) -> int:
-        n = 1
-        for s in self.segments:
-            n *= s
-        return n
+        return len(self.phase_a)
 
     @property
     def inverted_tiles(self) -> int:
-        n = 1
-        for s in self.segments:
-            n *= 2 * s
-        return n - self.upright_tiles
+        return len(self.phase_b)
+
+
+def axis_range(plan: TilePlan, axis: int, kind: str, index: int, step: int):
+    """tiling.cpp:20-31: cells owned on `axis` by a piece at 0-based step
+    `step` of a round, as (lo, hi)."""
+    shift = step * plan.radius
+    if kind == UPRIGHT:
+        lo = index * plan.tile[axis] + shift
+        last = index == plan.segments[axis] - 1
+        hi = plan.extent[axis] if last else (index + 1) * plan.tile[axis]
+        if not last:
+            hi -= shift
+        return lo, max(lo, hi)
+    anchor = index * plan.tile[axis]
+    return max(0, anchor - shift), min(plan.extent[axis], anchor + shift)
+
+
+def tile_range(plan: TilePlan, t: Tile, step: int):
+    """tiling.cpp:33-45: the owned box of a tile at a step, (lo, hi) lists."""
+    r = [axis_range(plan, a, t.kind[a], t.index[a], step) for a in range(plan.dims)]
+    return [x[0] for x in r], [x[1] for x in r]
+
+
+def count_coverage(plan: TilePlan):
+    """tiling.cpp:112-135 / module.cpp:190-193: ownership count of every
+    (cell, step) over both phases -> (all_ones, min_count, max_count).  A
+    correct plan owns every cell exactly once per step."""
+    import numpy as np
+    counts = np.zeros([plan.tb] + plan.extent, dtype=np.int32)
+    for t in plan.phase_a + plan.phase_b:
+        for s in range(plan.tb):
+            lo, hi = tile_range(plan, t, s)
+            counts[(s,) + tuple(slice(l, h) for l, h in zip(lo, hi))] += 1
+    mn, mx = int(counts.min()), int(counts.max())
+    return mn == 1 and mx == 1, mn, mx
 
 
 def plan_tiles(extent, spatial_tile, tb: int, radius: int) -> TilePlan:
-    """tiling.cpp:48-72 validation + segment counts."""
+    """tiling.cpp:48-102: validation, segment counts and the tile lists."""
     extent = [int(e) for e in extent]
     spatial_tile = [int(t) for t in spatial_tile]
     if not extent or len(extent) > 3:

@@ -94,3 +94,33 @@ def test_desk_scale_study_matches_reference(ts, ref, tmp_path):
     res = _check_against_reference(ts, ref, CaseStudyConfig(), tmp_path,
                                    threads=os.cpu_count() or 1)
     assert len(res["center_series"]) == 9500 // 25 + 1
+
+
+@pytest.mark.gpu
+def test_snapshot_and_resume_reproduce_the_run(ts, tmp_path):
+    """TTRS snapshots of the device fields every 150 steps; resuming from the
+    step-150 snapshots reproduces the rest of the uninterrupted run exactly:
+    centre series, checkpoint table and final.ttrs (grid_io.cpp:34-68)."""
+    import shutil
+    from paper_2303_08365_b200.case_study import CaseStudyConfig, case_study_heat
+    cfg = CaseStudyConfig(extent=96, steps=300, checkpoints=[100, 300], sample_every=50,
+                          snapshot_every=150)
+    full = case_study_heat(cfg, str(tmp_path / "full"))
+    assert (tmp_path / "full" / "snapshot_150_fp64.ttrs").exists()
+    (tmp_path / "resumed").mkdir()
+    for name in ("snapshot_150_fp64.ttrs", "snapshot_150_fp32.ttrs"):
+        shutil.copy(tmp_path / "full" / name, tmp_path / "resumed" / name)
+    part = case_study_heat(cfg, str(tmp_path / "resumed"), resume_step=150)
+    k = full["series_steps"].index(150)
+    assert part["series_steps"] == full["series_steps"][k:]
+    assert part["center_series"] == full["center_series"][k:]
+    assert part["checkpoint_steps"] == [300]
+    got, want = part["checkpoint_errors"][0], full["checkpoint_errors"][-1]
+    assert got.abs_exceed_pct == want.abs_exceed_pct and got.rel_exceed_pct == want.rel_exceed_pct
+    assert ((tmp_path / "resumed" / "final.ttrs").read_bytes() ==
+            (tmp_path / "full" / "final.ttrs").read_bytes())
+    # a snapshot is the device state itself: resuming it and snapshotting again is identity
+    dg = ts.DeviceGrid.resume(str(tmp_path / "full" / "snapshot_300_fp32.ttrs"), dtype="f32")
+    dg.snapshot(str(tmp_path / "again.ttrs"))
+    assert ((tmp_path / "again.ttrs").read_bytes() ==
+            (tmp_path / "full" / "snapshot_300_fp32.ttrs").read_bytes())

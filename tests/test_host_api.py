@@ -160,3 +160,21 @@ def test_gpu_entry_points_fail_loudly_without_a_device(ts):
     with pytest.raises(RuntimeError, match="CUDA"):
         ts.naive_run(g, ts.heat_coefficients(0.2), 2)
     assert g.parity == 0
+
+
+@pytest.mark.parametrize("extent,tile,tb", [([64, 64], [20, 20], 3), ([200, 37], [50, 12], 4),
+                                            ([20, 21, 23], [6, 6, 7], 2), ([97], [10], 5),
+                                            ([30, 31, 32], [10, 10, 10], 5)])
+def test_tile_plan_matches_reference(ts, ref, extent, tile, tb):
+    """plan_tiles' phase A / phase B lists (kind, index, wave, in order) and
+    count_coverage's (all_ones, min, max) are the reference's
+    (tiling.cpp:48-135, module.cpp:180-193)."""
+    p = ts.plan_tiles(extent, tile, tb, 1)
+    up, inv, cov, tiles = ref.plan_tiles(extent, tile, tb, 1)
+    assert (p.upright_tiles, p.inverted_tiles) == (up, inv)
+    assert [(t.kind, t.index, t.wave) for t in p.phase_a + p.phase_b] == tiles
+    assert ts.count_coverage(p) == cov == (True, 1, 1)
+    for t in p.phase_b[:3]:
+        for s in range(tb):
+            lo, hi = ts.tile_range(p, t, s)
+            assert all(0 <= l <= h <= e for l, h, e in zip(lo, hi, extent))
