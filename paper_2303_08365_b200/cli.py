@@ -2,9 +2,11 @@
 rebuilt on argparse (its CLI11 dependency is not vendored) over the GPU path.
 
     python -m paper_2303_08365_b200 list
-    python -m paper_2303_08365_b200 run [--name Heat-2D|a,b|all] [--path gpu|tessellate|naive]
+    python -m paper_2303_08365_b200 run [--name Heat-2D|a,b|all]
+                                        [--path gpu|tessellate|naive|hetero]
                                         [--scale desk|full] [--seed S] [--steps T]
                                         [--no-verify] [--out report.csv] [--mode exact|fast]
+                                        [--comm-log rounds.csv]
     python -m paper_2303_08365_b200 case-study [--config FILE] [--path P] [--full] [--out DIR]
 
 Same subcommands, options, output and exit codes as the reference: `run`
@@ -41,8 +43,11 @@ def _cmd_run(a, out) -> int:
     rows = []
     out.write(csv_header() + "\n")
     for n in names:
+        log = None
+        if a.comm_log and a.path == "hetero":  # one CommLog CSV per benchmark
+            log = a.comm_log if len(names) == 1 else a.comm_log.replace(".csv", "") + f"_{n}.csv"
         rows.append(run_benchmark(n, path=a.path, scale=a.scale, seed=a.seed, steps=a.steps,
-                                  mode=a.mode, verify=not a.no_verify))
+                                  mode=a.mode, verify=not a.no_verify, comm_log=log))
         out.write(csv_row(rows[-1]) + "\n")
         out.flush()
     if a.out:
@@ -76,8 +81,8 @@ def parser() -> argparse.ArgumentParser:
     sub = ap.add_subparsers(dest="cmd", required=True)
     r = sub.add_parser("run", help="time benchmarks on an executor path")
     r.add_argument("--name", default="Heat-2D", help="benchmark name, comma list, or 'all'")
-    r.add_argument("--path", default="gpu", help="gpu|tessellate|naive (vector|mm|hetero: "
-                   "CPU simulators of the reference, reported unsupported)")
+    r.add_argument("--path", default="gpu", help="gpu|tessellate|naive|hetero (two GPU slabs; "
+                   "vector|mm: CPU simulators of the reference, reported unsupported)")
     r.add_argument("--scale", default="desk", choices=["desk", "full"])
     r.add_argument("--threads", type=int, default=1, help="accepted, ignored")
     r.add_argument("--seed", type=int, default=1)
@@ -85,6 +90,8 @@ def parser() -> argparse.ArgumentParser:
     r.add_argument("--no-verify", action="store_true", help="skip the reduced-size check")
     r.add_argument("--out", default="", help="CSV report path")
     r.add_argument("--mode", default="exact", choices=["exact", "fast"])
+    r.add_argument("--comm-log", default="", help="hetero: per-round CommLog CSV "
+                   "(round,direction,bytes,modeled_cost_alpha_beta,wall_seconds)")
     c = sub.add_parser("case-study", help="thermal diffusion on a square plate")
     c.add_argument("--config", default="", help="line-oriented key = value config file")
     c.add_argument("--path", default="", help="executor path override")

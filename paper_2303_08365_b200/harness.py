@@ -8,7 +8,11 @@ first verified at a reduced size, then timed at desk or full scale:
 
 * paths ``gpu`` (engine's fused depth), ``tessellate`` (k = the Table-1 tb,
   clamped like clamp_tb, bench.cpp:104-107) and ``naive`` (k = 1) run on the
-  B200; ``vector``/``mm``/``hetero`` are CPU simulators of the reference and
+  B200; ``hetero`` is the reference's two-worker deep-halo partition
+  (bench.cpp:169-189: profile_workers on a <= 64^d sample, plan_partition,
+  run_heterogeneous) on two GPU slabs, with its CommLog's message count and
+  ghost recompute in the row (``comm_log=`` writes the per-round CSV,
+  dump_comm_log); ``vector``/``mm`` are CPU simulators of the reference and
   report ``unsupported``, like its unsupported path/dimension pairings;
 * verify compares the tuned engine with the one-thread-per-point generic GPU
   engine (an independent implementation of apply_box; the product never
@@ -27,8 +31,8 @@ from .kernel import benchmark_table, find_benchmark
 from .metrics import deviation, stencils_per_second
 from .run import run_gpu
 
-PATHS = ("gpu", "tessellate", "naive")
-CPU_ONLY = ("vector", "mm", "hetero")
+PATHS = ("gpu", "tessellate", "naive", "hetero")
+CPU_ONLY = ("vector", "mm")
 
 
 def clamp_tb(tb: int, min_tile: int, radius: int) -> int:
@@ -55,7 +59,20 @@ def verify_setup(spec):
 
 
 def _fused(path: str, tb: int) -> int:
-    return {"gpu": 0, "tessellate": tb, "naive": 1}[path]
+    return {"gpu": 0, "tessellate": tb, "naive": 1, "hetero": tb}[path]
+
+
+def _hetero(g, k, steps: int, extent, tile, tb: int, mode: str):
+    """bench.cpp:169-189 on two GPU slabs: the workers are profiled on a
+    sample of at most 64 cells per axis, the plan splits axis 0 on a tile
+    multiple, run_heterogeneous advances the grid; returns its CommLog."""
+    from .scheduler import (WorkerSpec, plan_partition, profile_workers, run_heterogeneous)
+    cpu = WorkerSpec("cpu_like", "tessellate")
+    accel = WorkerSpec("accel_like", "mm" if k.dims == 2 else "naive")
+    pc, pa = profile_workers(cpu, accel, k, [min(e, 64) for e in extent], 1)
+    plan = plan_partition(pc, pa, extent, tile[0], tb, k.radius)
+    first, second = (cpu, accel) if plan.first_worker == "cpu_like" else (accel, cpu)
+    return run_heterogeneous(g, k, steps, plan, first, second, mode=mode)
 
 
 def _hbm_peak_gbps() -> float:
@@ -74,7 +91,7 @@ def _hbm_peak_gbps() -> float:
 
 def run_benchmark(name: str, path: str = "gpu", scale: str = "desk", threads: int = 1,
                   seed: int = 1, steps: int = 0, mode: str = "exact",
-                  verify: bool = True) -> dict:
+                  verify: bool = True, comm_log: str | None = None) -> dict:
     spec = find_benchmark(name)
     k = spec.kernel
     row = {"name": spec.name, "path": path, "dims": k.dims, "extent": [], "T": 0, "tile": [],
@@ -96,7 +113,10 @@ def run_benchmark(name: str, path: str = "gpu", scale: str = "desk", threads: in
         probe = Grid(vext, [k.radius] * k.dims)
         fill_random(probe, seed)
         check = probe.copy()
-        run_gpu(probe, k, 6, fused_steps=_fused(path, vtb), mode=mode)
+        if path == "hetero":
+            _hetero(probe, k, 6, vext, verify_setup(spec)[1], vtb, mode)
+        else:
+            run_gpu(probe, k, 6, fused_steps=_fused(path, vtb), mode=mode)
         run_gpu(check, k, 6, engine="generic")
         d = deviation(probe, check)
         row["verify"] = "pass" if d["max_rel_deviation"] <= 1e-12 else "fail"
@@ -115,6 +135,18 @@ def run_benchmark(name: str, path: str = "gpu", scale: str = "desk", threads: in
     run_gpu(warm, k, 2 * max(_fused(path, tb), 1) + 1, fused_steps=_fused(path, tb), mode=mode)
     g = Grid(extent, [k.radius] * k.dims, pinned=True)
     fill_random(g, seed)
+    if path == "hetero":
+        t0 = time.perf_counter()
+        log = _hetero(g, k, t_steps, extent, tile, tb, mode)
+        elapsed = max(time.perf_counter() - t0, 1e-9)
+        rate = stencils_per_second(extent, t_steps, elapsed)
+        row.update(elapsed_s=elapsed, stencils_per_s=rate.stencils_per_second, k=tb, gpus=2,
+                   messages=log.messages, ghost_recompute_points=log.ghost_recompute_points,
+                   device_s=sum(r.wall_seconds for r in log.records))
+        if comm_log:
+            from .scheduler import dump_comm_log
+            dump_comm_log(comm_log, log)
+        return row
     t0 = time.perf_counter()
     st = run_gpu(g, k, t_steps, fused_steps=_fused(path, tb), mode=mode)
     elapsed = max(time.perf_counter() - t0, 1e-9)

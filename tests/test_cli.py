@@ -27,7 +27,7 @@ def test_errors_exit_1(capsys):
 
 
 def test_cpu_only_paths_report_unsupported(ts):
-    """vector/mm/hetero are the reference's CPU simulators: rows say so."""
+    """vector/mm are the reference's CPU simulators: rows say so."""
     from paper_2303_08365_b200.cli import main
     out = io.StringIO()
     assert main(["run", "--name", "Heat-2D,Heat-3D", "--path", "mm"], out) == 0

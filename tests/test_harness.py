@@ -36,3 +36,29 @@ def test_benchmark_rows_verify_and_time(ts, path):
         row = ts.run_benchmark(spec.name, path=path, steps=4, seed=7)
         assert row["verify"] == "pass", row
         assert row["stencils_per_s"] > 0 and row["T"] == 4 and row["k"] >= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["Heat-2D", "Heat-3D", "Box-3D27P"])
+def test_hetero_path_rows_and_comm_log(ts, orc, ref, name, tmp_path):
+    """--path hetero (bench.cpp:169-189) on two GPU slabs: the row verifies
+    against the generic engine, its message count and ghost recompute are
+    the reference run_heterogeneous's on the same grid, tile and tb, and the
+    CLI writes the per-round CommLog CSV (scheduler.cpp:152-159)."""
+    from paper_2303_08365_b200 import harness as h
+    from paper_2303_08365_b200.cli import main
+    import io
+    spec = ts.find_benchmark(name)
+    row = ts.run_benchmark(name, path="hetero", steps=7, seed=3)
+    assert row["verify"] == "pass" and row["gpus"] == 2, row
+    extent, tile, tb = h.make_setup(spec, "desk")
+    g = ts.Grid(extent, [1] * len(extent))
+    orc.fill_random(g, 3)
+    msgs, ghost, _, _ = ref.run_heterogeneous(g, spec.kernel, 7, tile[0], tb)
+    assert (row["messages"], row["ghost_recompute_points"]) == (msgs, ghost)
+    csv = tmp_path / "rounds.csv"
+    assert main(["run", "--name", name, "--path", "hetero", "--steps", "7",
+                 "--comm-log", str(csv)], io.StringIO()) == 0
+    lines = csv.read_text().splitlines()
+    assert lines[0] == "round,direction,bytes,modeled_cost_alpha_beta,wall_seconds"
+    assert len(lines) == 1 + msgs
