@@ -140,7 +140,12 @@ def run_benchmark(name: str, path: str = "gpu", scale: str = "desk", threads: in
         log = _hetero(g, k, t_steps, extent, tile, tb, mode)
         elapsed = max(time.perf_counter() - t0, 1e-9)
         rate = stencils_per_second(extent, t_steps, elapsed)
-        row.update(elapsed_s=elapsed, stencils_per_s=rate.stencils_per_second, k=tb, gpus=2,
+        # the slabs exchange every k = min(tb, engine max) steps: the GPU's
+        # deep halo is r*k planes, not r*tb (same bits, more frequent rounds)
+        from . import _abi
+        _, k_used = _abi.query_plan(k, _abi.grid_desc(extent, [k.radius] * k.dims, "f64"), tb,
+                                    mode)
+        row.update(elapsed_s=elapsed, stencils_per_s=rate.stencils_per_second, k=k_used, gpus=2,
                    messages=log.messages, ghost_recompute_points=log.ghost_recompute_points,
                    device_s=sum(r.wall_seconds for r in log.records))
         if comm_log:

@@ -43,8 +43,10 @@ def test_benchmark_rows_verify_and_time(ts, path):
 def test_hetero_path_rows_and_comm_log(ts, orc, ref, name, tmp_path):
     """--path hetero (bench.cpp:169-189) on two GPU slabs: the row verifies
     against the generic engine, its message count and ghost recompute are
-    the reference run_heterogeneous's on the same grid, tile and tb, and the
-    CLI writes the per-round CommLog CSV (scheduler.cpp:152-159)."""
+    the reference run_heterogeneous's on the same grid and tile with the
+    round length the GPU slabs use (tb clamped to the engine's fused depth:
+    the deep halo is r*k planes), and the CLI writes the per-round CommLog
+    CSV (scheduler.cpp:152-159)."""
     from paper_2303_08365_b200 import harness as h
     from paper_2303_08365_b200.cli import main
     import io
@@ -54,7 +56,8 @@ def test_hetero_path_rows_and_comm_log(ts, orc, ref, name, tmp_path):
     extent, tile, tb = h.make_setup(spec, "desk")
     g = ts.Grid(extent, [1] * len(extent))
     orc.fill_random(g, 3)
-    msgs, ghost, _, _ = ref.run_heterogeneous(g, spec.kernel, 7, tile[0], tb)
+    assert 1 <= row["k"] <= tb
+    msgs, ghost, _, _ = ref.run_heterogeneous(g, spec.kernel, 7, tile[0], row["k"])
     assert (row["messages"], row["ghost_recompute_points"]) == (msgs, ghost)
     csv = tmp_path / "rounds.csv"
     assert main(["run", "--name", name, "--path", "hetero", "--steps", "7",
