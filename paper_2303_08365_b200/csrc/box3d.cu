@@ -406,7 +406,10 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
         for (int r = 0; r < VY + 2; ++r) load_row<T, NLX>(rowbase + (y + r) * pitch, x, lx, nb[r]);
     };
 
-    for (int it = 0; it < niter; ++it) {
+    // output plane q-2 of step it, advanced by one plane per step
+    T* orow2 = out + (a.origin + (long long)(t_begin - 2) * a.pitch0 +
+                      (long long)(gy + y) * a.pitch1 + (gx + x));
+    for (int it = 0; it < niter; ++it, orow2 += a.pitch0) {
         const int q = t_begin + it;  // level-0 plane in the ring
         const int slot = it % STAGES;
         mbar_wait(&bar[slot], (it / STAGES) & 1);
@@ -499,8 +502,7 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
         const int po = q - 2;
         if (it >= 4 && po < i1) {
             // stored cells are interior (cout implies cint): no Dirichlet select
-            T* o = out + a.origin + (long long)po * a.pitch0 + (long long)(gy + y) * a.pitch1 +
-                   (gx + x);
+            T* o = orow2;
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy) {
                 T v[VX];

@@ -128,9 +128,10 @@ __device__ __forceinline__ void store_row(T* o, const T (&v)[N], const bool (&ok
     static_assert(N % NV == 0, "row length must be a multiple of the vector");
 #pragma unroll
     for (int c = 0; c < N; c += NV) {
-        bool all = true;
+        bool all = true, any = false;
 #pragma unroll
-        for (int u = 0; u < NV; ++u) all &= ok[c + u];
+        for (int u = 0; u < NV; ++u) all &= ok[c + u], any |= ok[c + u];
+        if (!any) continue;  // lanes outside the output tile skip the scalar path too
         if (all) {
             if constexpr (sizeof(T) == 8 && NV == 2) {
                 *reinterpret_cast<double2*>(o + c) = make_double2(v[c], v[c + 1]);
