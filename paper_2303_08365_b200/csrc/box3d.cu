@@ -37,7 +37,8 @@ constexpr int BY = OY + 2;
 template <typename T>
 constexpr int PAD = 16 / (int)sizeof(T);  // 16-B aligned box start / rows
 template <typename T>
-constexpr int BXW = OX + 2 * PAD<T>;
+constexpr int BXW = OX + 3 * PAD<T>;  // k=2 box: one spare vector so rows 4 apart
+                                      // (the two half-warps) fall in other banks
 template <typename T>
 constexpr int slot_bytes() {
     return (BXW<T> * BY * (int)sizeof(T) + 127) / 128 * 128;
@@ -320,7 +321,7 @@ template <typename T>
 constexpr int TX2 = (L1X - HX2<T> - 1) / PAD<T> * PAD<T>;            // output width
 constexpr int TY2 = L1Y - 2;                                         // output height
 template <typename T>
-constexpr int BWP = L1X + 2 * PAD<T>;                                // SMEM row pitch
+constexpr int BWP = L1X + 3 * PAD<T>;  // SMEM row pitch (+1 vector: conflict-free edges)
 
 template <typename T>
 constexpr int b_bytes() {
