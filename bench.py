@@ -28,10 +28,10 @@ N=1 line carries `modes`: the EXACT mode (mul + add per tap, bitwise
 naive_run) timed on the same input, plus the full-grid max_rel_deviation and
 a bitwise flag between the two.  Heat-3D's weights (1/4, 1/8) are powers of
 two, so its products are exact and FAST is bitwise EXACT on normal-range data
-(the flag shows it).  C4's FAST mode is the separable box sum (row, column
-and plane sums times the one 1/27 weight: 8 operations per update, two fused
-steps per pass), reported with its max_rel_deviation from EXACT (<= 1e-5).
-C2 runs EXACT: its shared-product Q mode is as fast as FMA.
+(the flag shows it).  The box kernels' FAST mode is the separable box sum
+(row, column and plane sums times the one weight: C4 8 operations per update
+at two fused steps per pass, C2 4.5 instead of Q mode's 9), reported with its
+max_rel_deviation from EXACT (<= 1e-5 fp32, <= 1e-12 fp64).
 
 `value` is device-resident throughput (GStencil/s = points * K / time, the
 reference's Eq. 6, proj/src/metrics.cpp:8-20), timed with CUDA events on the
@@ -64,7 +64,7 @@ CONFIGS = {
                mode="fast", workload="C1: 2D heat 5-point star fp64, 4096x4096, 100 timesteps",
                ref_tile=[200, 200], ref_tb=50),
     "c2": dict(bench="Box-2D9P", extent=[16384, 16384], dtype="f64", steps=100, fused=4,
-               mode="exact",
+               mode="fast",
                workload="C2: 2D 9-point box fp64, 16384x16384, temporal blocking k=4",
                ref_tile=[2000, 2000], ref_tb=4),
     "c3": dict(bench="Heat-3D", extent=[512, 512, 512], dtype="f64", steps=1000, fused=0,

@@ -115,6 +115,20 @@ __device__ __forceinline__ void exchange(T (&row)[V + 2 * R]) {
     }
 }
 
+// SEP: horizontal 3-sums of one window row (its V values at [1, V+1), the
+// outer neighbours from the adjacent lanes), consecutive pairs shared.
+template <typename T, int V>
+__device__ __forceinline__ void hsum(const T (&row)[V + 2], T (&h)[V]) {
+    const T left = __shfl_up_sync(0xffffffffu, row[V], 1);
+    const T right = __shfl_down_sync(0xffffffffu, row[1], 1);
+#pragma unroll
+    for (int v = 0; v < V; v += 2) {
+        const T m = row[1 + v] + row[2 + v];
+        h[v] = (v == 0 ? left : row[v]) + m;
+        h[v + 1] = m + (v + 2 == V ? right : row[3 + v]);
+    }
+}
+
 // MODE: 0 = FAST (FMA per tap), 1 = EXACT (multiply, then add, per tap),
 // 2 = Q (exact, for kernels whose taps all carry one weight w, e.g. the
 // reference's Box-2D9P / Box-2D25P): the level windows hold q = w*v, the
@@ -124,8 +138,14 @@ __device__ __forceinline__ void exchange(T (&row)[V + 2 * R]) {
 template <typename T, int R, bool BOX, int K, int V, int MODE>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     const T* __restrict__ in, T* __restrict__ out, const __grid_constant__ S2Args<T> a) {
-    constexpr bool EXACT = MODE != 0;
+    constexpr bool EXACT = MODE == 1 || MODE == 2;
     constexpr bool QS = MODE == 2;
+    // MODE 3 = SEP (FAST, uniform-weight 9-point box): the windows hold each
+    // row's raw values and its horizontal 3-sums h; an update is
+    // w * ((h[x-1] + h[x]) + h[x+1]): 2 adds + 1 multiply, plus 1.5 adds per
+    // produced value for its h, instead of 9 adds (Q) — within 1e-12.
+    constexpr bool SEP = MODE == 3;
+    static_assert(!SEP || (BOX && R == 1), "SEP serves the 9-point box");
     constexpr int P = 2 * R + 1;  // ring depth per level
     constexpr int W = V + 2 * R;  // values per ring row incl. lane halo
     const int lane = threadIdx.x & 31;
@@ -152,6 +172,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     for (int v = 0; v < V; ++v) all_out &= cout[v];
 
     T win[K][P][W];  // ring of rows per level (level K is stored, not kept)
+    T hwin[SEP ? K : 1][P][V];  // SEP: horizontal 3-sums of the window rows
     // staging ring of level-0 rows: kDepth + 1 slots, row t in slot
     // (t - t_start) % (kDepth + 1); a slot is refilled one step after it was
     // read, so a lane never overwrites data it has not consumed
@@ -163,7 +184,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
     // whose updates are pure add chains and latency-bound): every row a
     // level reads was produced in an earlier step, so the K levels of a step
     // are independent chains (levels run in descending order, level 0 last).
-    constexpr bool SKEW = QS && R == 1;  // (the 25-point box measured slower skewed)
+    constexpr bool SKEW = (QS || SEP) && R == 1;  // (the 25-point box measured slower skewed)
     constexpr int S = SKEW ? R + 1 : R;
     const int64_t t_start = rb - (int64_t)K * R;  // first level-0 row of the cone
     const int64_t t_end = re + (int64_t)K * S;    // exclusive: level K stores row re-1
@@ -208,7 +229,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
 #pragma unroll
         for (int v = 0; v < V; ++v) win[0][ph][R + v] = QS ? mul_rn(a.w[0], rv[v]) : rv[v];
         fetch();  // row t + kDepth, into the slot row t-1 vacated
-        if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
+        if constexpr (SEP) hsum<T, V>(win[0][ph], hwin[0][ph]);
+        else if constexpr (BOX) exchange<T, V, R>(win[0][ph]);
     };
 
     // One row step: level 0 takes row t, level l produces row t - l*S.
@@ -230,6 +252,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
             T res[V];
 #pragma unroll
             for (int v = 0; v < V; ++v) {
+                if constexpr (SEP) {
+                    const int sm = (sx + P - 1) % P, sp = (sx + 1) % P;
+                    T nv = a.w[0] * ((hwin[l - 1][sm][v] + hwin[l - 1][sx][v]) + hwin[l - 1][sp][v]);
+                    if constexpr (SEL) {
+                        const bool rint = x >= 0 && x < a.rows;
+                        if (l < K) nv = (rint && cint[v]) ? nv : win[l - 1][sx][R + v];
+                    }
+                    res[v] = nv;
+                    continue;
+                }
                 T acc = T(0);
                 int tap = 0;
 #pragma unroll
@@ -259,7 +291,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
             if (l < K) {
 #pragma unroll
                 for (int v = 0; v < V; ++v) win[l][sx][R + v] = res[v];
-                if constexpr (BOX) exchange<T, V, R>(win[l][sx]);
+                if constexpr (SEP) hsum<T, V>(win[l][sx], hwin[l][sx]);
+                else if constexpr (BOX) exchange<T, V, R>(win[l][sx]);
             } else if (x >= rb && x < re) {
 #pragma unroll
                 for (int v = 0; v < V; ++v) res[v] = fix_zero<EXACT>(res[v]);
@@ -352,7 +385,16 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     const unsigned blocks =
         static_cast<unsigned>((a.total_warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
     if constexpr (BOX) {
-        if (uniform_weights(*c.taps)) {  // Q mode serves exact and fast alike
+        if (uniform_weights(*c.taps)) {  // Q mode (exact), separable sums in FAST (R = 1)
+            if constexpr (R == 1) {
+                if (!c.exact) {
+                    stream2d_kernel<T, R, BOX, K, V, 3>
+                        <<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
+                            static_cast<const T*>(in), static_cast<T*>(out), a);
+                    TSR_CUDA_TRY(cudaGetLastError());
+                    return Status::Ok();
+                }
+            }
             stream2d_kernel<T, R, BOX, K, V, 2><<<blocks, 32 * kWarpsPerBlock, 0, c.stream>>>(
                 static_cast<const T*>(in), static_cast<T*>(out), a);
             TSR_CUDA_TRY(cudaGetLastError());

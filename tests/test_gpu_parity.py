@@ -454,6 +454,13 @@ def test_reduced_shape_full_steps(ts, orc, cfg):
     st = ts.run_gpu(got, k, steps, fused_steps=fused, mode="exact")
     assert st.fused_steps == fused
     assert both_buffers_equal(got, ref)
+    if cfg == "c2":  # FAST = separable 9-point sums, several fused depths
+        for kf in (1, 4, 7):
+            fast = a.copy()
+            st = ts.run_gpu(fast, k, steps, fused_steps=kf, mode="fast")
+            assert st.fused_steps == kf
+            d = ts.deviation(fast, ref)
+            assert d["max_rel_deviation"] <= TOL["f64"] and d["l2_rel_err"] <= TOL["f64"], (kf, d)
     if cfg == "c4":  # FAST = separable box sums (uniform weights), one and two levels
         for kf in (1, 2):
             fast = a.copy()
