@@ -7,6 +7,10 @@
 //   naive_run        proj/include/tessera/naive.hpp:96-100
 //   naive_step       proj/include/tessera/naive.hpp:89-94
 //   run_tessellated  proj/include/tessera/tiling.hpp:82-83
+//   run_heterogeneous proj/include/tessera/scheduler.hpp:109-113 (two GPU
+//                    slabs, the reference's PartitionPlan / WorkerSpec /
+//                    CommLog / HeteroMode / CommCostModel)
+// plus run_multi (P slabs on P GPUs from this thread, tsr_run_multi),
 // and errors surface as the same std exceptions (std::invalid_argument for
 // bad arguments, std::runtime_error for device failures).  The grid is left
 // exactly as the reference leaves it: parity flipped `steps` times, both
@@ -17,6 +21,7 @@
 // taps), so this header does not include the reference's headers.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <new>
 #include <stdexcept>
@@ -137,6 +142,159 @@ void run_tessellated(Grid& g, const Kernel& k, std::int64_t steps, const Plan& p
             stats->rounds = steps / plan.tb;
             stats->trailing_steps = steps % plan.tb;
         }
+    }
+}
+
+// ---- slabs on several GPUs (tsr_run_multi / tsr_multi_*) ----------------
+
+struct MultiOptions : GpuOptions {
+    std::vector<int32_t> devices;          // slab i on devices[i]; empty = i mod device count
+    std::vector<std::int64_t> boundaries;  // ngpus-1 ascending axis-0 boundaries; empty = equal
+    int transport = TSR_XPORT_AUTO;
+    bool keep_previous = true;  // both buffers as naive_run leaves them; false: only the final
+                                // read buffer is written (run_heterogeneous's post-condition)
+};
+
+inline tsr_partition partition_of(int ngpus, const MultiOptions& o, int flags = 0) {
+    tsr_partition p{};
+    p.ngpus = ngpus;
+    p.split_axis = 0;
+    p.devices = o.devices.empty() ? nullptr : o.devices.data();
+    p.boundaries = o.boundaries.empty() ? nullptr : o.boundaries.data();
+    p.transport = o.transport;
+    p.flags = flags;
+    return p;
+}
+
+// naive_run over `ngpus` slabs of axis 0 in one call: host buffers in, host
+// buffers out, the grid left as naive_run leaves it (keep_previous).
+template <class Grid, class Kernel>
+GpuStats run_multi(Grid& g, const Kernel& k, std::int64_t steps, int ngpus,
+                   const MultiOptions& o = {}) {
+    if (steps < 0) throw std::invalid_argument("negative step count");
+    if (ngpus < 1) throw std::invalid_argument("ngpus must be >= 1");
+    const KernelView kv(k);
+    const tsr_grid gd = grid_desc(g);
+    tsr_opts opts{};
+    opts.fused_steps = o.fused_steps;
+    opts.mode = o.exact ? TSR_EXACT : TSR_FAST;
+    opts.engine = o.engine;
+    opts.device = -1;
+    opts.ngpus = ngpus;
+    const tsr_partition part = partition_of(ngpus, o);
+    GpuStats st{};
+    throw_status(tsr_run_multi(kv.get(), &gd, g.buffer(0), g.buffer(1), g.parity(), steps, &part,
+                               o.keep_previous ? 1 : 0, &opts, &st));
+    if (steps & 1) g.flip_parity();
+    return st;
+}
+
+namespace detail {
+template <class M, class = void>
+struct has_alpha_beta : std::false_type {};
+template <class M>
+struct has_alpha_beta<M, std::void_t<decltype(std::declval<const M&>().alpha),
+                                     decltype(std::declval<const M&>().beta)>> : std::true_type {};
+
+// The reference's run_heterogeneous_impl (scheduler.cpp:441-563) on two GPU
+// slabs split at plan.boundary, rounds of plan.tb steps (clamped to the
+// engine's fused depth), deep halo r*k; the CommLog gets one record per
+// seam delivery (round, "w0_to_w1" / "w1_to_w0", bytes, alpha-beta cost,
+// the sender's seam-pass device time) and the ghost recompute tally.
+template <class Grid, class Kernel, class Plan, class Log>
+void hetero(Grid& g, const Kernel& k, std::int64_t steps, const Plan& plan, Log* log,
+            double alpha, double beta, bool poison) {
+    // the reference's checks, in its order
+    if (g.dims() != k.dims()) throw std::invalid_argument("kernel/grid dimensionality mismatch");
+    for (int a = 0; a < g.dims(); ++a)
+        if (g.halo(a) < k.radius()) throw std::invalid_argument("grid halo too small for kernel radius");
+    if (steps < 0) throw std::invalid_argument("negative step count");
+    if (k.radius() != plan.radius)
+        throw std::invalid_argument("partition plan radius differs from kernel radius");
+    if (plan.halo_depth != static_cast<std::int64_t>(plan.radius) * plan.tb)
+        throw std::invalid_argument("partition plan halo depth must be radius*tb");
+    const std::int64_t n = g.extent(0), b = plan.boundary;
+    if (b <= 0 || b >= n) throw std::invalid_argument("partition boundary outside the grid");
+    if (b < plan.halo_depth || n - b < plan.halo_depth)
+        throw std::invalid_argument("subdomain smaller than the halo depth");
+    if (log) *log = Log{};
+    if (steps == 0) return;
+
+    const KernelView kv(k);
+    const tsr_grid gd = grid_desc(g);
+    tsr_opts opts{};
+    opts.fused_steps = plan.tb;
+    opts.mode = TSR_EXACT;
+    opts.engine = TSR_ENGINE_AUTO;
+    opts.device = -1;
+    opts.ngpus = 2;
+    MultiOptions mo;
+    mo.boundaries = {b};
+    const tsr_partition part = partition_of(2, mo, poison ? TSR_PART_POISON : 0);
+    tsr_multi* m = nullptr;
+    throw_status(tsr_multi_create(kv.get(), &gd, &part, &opts, &m));
+    struct Guard {
+        tsr_multi* m;
+        ~Guard() { tsr_multi_destroy(m); }
+    } guard{m};
+    throw_status(tsr_multi_upload(m, g.buffer(g.parity())));
+    throw_status(tsr_multi_set_logging(m, log ? 1 : 0));
+    GpuStats st{};
+    throw_status(tsr_multi_advance(m, steps, 0, &st));
+    if (steps & 1) g.flip_parity();
+    // run_heterogeneous scatters the workers' rows into the final read
+    // buffer only (scheduler.cpp:555-557)
+    throw_status(tsr_multi_download(m, g.buffer(g.parity()), nullptr));
+    if (log) {
+        std::int64_t count = 0;
+        throw_status(tsr_multi_comm_log(m, nullptr, 0, &count));
+        std::vector<tsr_comm_record> recs(static_cast<size_t>(count));
+        throw_status(tsr_multi_comm_log(m, recs.data(), count, &count));
+        for (const tsr_comm_record& r : recs) {
+            typename std::decay_t<decltype(log->records)>::value_type c{};
+            c.round = r.round;
+            c.direction = "w" + std::to_string(r.from_slab) + "_to_w" + std::to_string(r.to_slab);
+            c.bytes = r.bytes;
+            c.modeled_cost_alpha_beta = alpha + static_cast<double>(r.bytes) * beta;
+            c.wall_seconds = r.seam_ms / 1e3;
+            log->records.push_back(c);
+        }
+        std::sort(log->records.begin(), log->records.end(), [](const auto& x, const auto& y) {
+            return x.round != y.round ? x.round < y.round : x.direction < y.direction;
+        });
+        log->ghost_recompute_points = st.ghost_recompute_points;
+    }
+}
+}  // namespace detail
+
+// run_heterogeneous (scheduler.hpp:109-113): the same call, the two workers
+// become two GPU slabs (the worker specs and the drive mode only select the
+// reference's CPU engines and threads; every GPU slab runs the tuned engine
+// from one host thread, which gives the same bits as both of its drives).
+template <class Grid, class Kernel, class Plan, class Worker, class Log = void, class Mode = int,
+          class Model = int>
+void run_heterogeneous(Grid& g, const Kernel& k, std::int64_t steps, const Plan& plan,
+                       const Worker& /*first*/, const Worker& /*second*/, Log* log = nullptr,
+                       Mode /*mode*/ = Mode{}, const Model& model = Model{}) {
+    double alpha = 1e-5, beta = 1e-9;  // CommCostModel defaults (scheduler.hpp:66-73)
+    if constexpr (detail::has_alpha_beta<Model>::value) {
+        alpha = model.alpha;
+        beta = model.beta;
+    }
+    if constexpr (std::is_void_v<Log>) {
+        struct NoRec {
+            std::int64_t round;
+            std::string direction;
+            std::int64_t bytes;
+            double modeled_cost_alpha_beta, wall_seconds;
+        };
+        struct NoLog {
+            std::vector<NoRec> records;
+            std::int64_t ghost_recompute_points = 0;
+        };
+        detail::hetero(g, k, steps, plan, static_cast<NoLog*>(nullptr), alpha, beta, false);
+    } else {
+        detail::hetero(g, k, steps, plan, log, alpha, beta, false);
     }
 }
 
