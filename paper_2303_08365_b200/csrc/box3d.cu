@@ -336,7 +336,7 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
                                                       const __grid_constant__ CUtensorMap tmap,
                                                       const __grid_constant__ BoxArgs<T> a) {
-    constexpr bool EXACT = MODE == 1 || MODE == 2, Q = MODE == 2, SEP = MODE == 3;
+    constexpr bool EXACT = MODE != 0, Q = MODE == 2;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
     constexpr int BE = b_bytes<T>() / (int)sizeof(T);
@@ -424,16 +424,7 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
                 for (int c = 0; c < VX + 2; ++c) nb[r][c] = mul_rn(a.w[0], nb[r][c]);
         }
         // level 1: finish q-1, continue q, start q+1
-        T ps[VY][VX];
-        if constexpr (SEP) {
-            plane_sum9(nb, ps);
-#pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
-#pragma unroll
-                for (int cx = 0; cx < VX; ++cx) a1B[cy][cx] = a.w[0] * (a1B[cy][cx] + ps[cy][cx]);
-        } else {
-            apply9<EXACT, false, T, Q>(a.w + 18, nb, a1B);
-        }
+        apply9<EXACT, false, T, Q>(a.w + 18, nb, a1B);
         T l1[VY][VX];
 #pragma unroll
         for (int cy = 0; cy < VY; ++cy)
@@ -451,22 +442,12 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
         for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < VX; ++cx) keep0[cy][cx] = nb[cy + 1][cx + 1];
-        if constexpr (SEP) {
+        apply9<EXACT, false, T, Q>(a.w + 9, nb, a1A);
 #pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
+        for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-                for (int cx = 0; cx < VX; ++cx) {
-                    a1B[cy][cx] = a1A[cy][cx] + ps[cy][cx];
-                    a1A[cy][cx] = ps[cy][cx];
-                }
-        } else {
-            apply9<EXACT, false, T, Q>(a.w + 9, nb, a1A);
-#pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
-#pragma unroll
-                for (int cx = 0; cx < VX; ++cx) a1B[cy][cx] = a1A[cy][cx];
-            apply9<EXACT, true, T, Q>(a.w, nb, a1A);
-        }
+            for (int cx = 0; cx < VX; ++cx) a1B[cy][cx] = a1A[cy][cx];
+        apply9<EXACT, true, T, Q>(a.w, nb, a1A);
         // publish level-1 plane q-1: cell (y, x) at row y+1, column x+PAD
         T* B = buf + (((q - 1) % NB + NB) % NB) * BE;
 #pragma unroll
@@ -490,16 +471,7 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
         // level 2 on level-1 plane q-1: finish q-2, continue q-1, start q
         T nb2[VY + 2][VX + 2];
         read_nb(B + PL + x, BW, nb2);  // buffer rows y..y+VY+1 = region rows y-1..y+VY
-        T ps2[VY][VX];
-        if constexpr (SEP) {
-            plane_sum9(nb2, ps2);
-#pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
-#pragma unroll
-                for (int cx = 0; cx < VX; ++cx) a2B[cy][cx] = a.w[0] * (a2B[cy][cx] + ps2[cy][cx]);
-        } else {
-            apply9<EXACT, false, T, Q>(a.w + 18, nb2, a2B);
-        }
+        apply9<EXACT, false, T, Q>(a.w + 18, nb2, a2B);
         const int po = q - 2;
         if (it >= 4 && po < i1) {
             // stored cells are interior (cout implies cint): no Dirichlet select
@@ -513,21 +485,210 @@ __global__ void __launch_bounds__(NT) box3d_tb2_kernel(T* __restrict__ out,
                 if (a.mirror) store_row<T, VX>(a.mirror + (o - out) + a.mshift + cy * a.pitch1, v, cout[cy]);
             }
         }
-        if constexpr (SEP) {
+        apply9<EXACT, false, T, Q>(a.w + 9, nb2, a2A);
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < VX; ++cx) a2B[cy][cx] = a2A[cy][cx];
+        apply9<EXACT, true, T, Q>(a.w, nb2, a2A);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k = KL levels in SEP mode (FAST, uniform weights), one __syncthreads per
+// plane: level l consumes the level-(l-1) plane published in the PREVIOUS
+// plane step (a lag of two planes per level, as tb3d's skew), so every read
+// of a step sees data published before its barrier.  Level 1 reads the TMA
+// ring; level l > 1 reads a two-slot SMEM plane of level l-1 (written at
+// step s, read at s+1, rewritten at s+2 after the barrier).  Each level
+// keeps the two open accumulators of the plane-sum recurrence (finish
+// p-1, continue p, start p+1 per consumed plane) and the previous consumed
+// centre for its Dirichlet cells.  Output plane of step it: q - (2KL - 1).
+template <int KL, typename T>
+constexpr int HXK = (KL - 1 + PAD<T> - 1) / PAD<T> * PAD<T>;  // left margin (>= KL-1, aligned)
+template <int KL, typename T>
+constexpr int TXK = (L1X - HXK<KL, T> - (KL - 1)) / PAD<T> * PAD<T>;  // output width
+template <int KL>
+constexpr int TYK = L1Y - 2 * (KL - 1);  // output height
+template <int KL, typename T>
+constexpr int smemk_bytes() {
+    return STAGES * slot_bytes<T>() + (KL - 1) * NB * b_bytes<T>() + STAGES * 8;
+}
+
+template <typename T, int KL>
+__global__ void __launch_bounds__(NT) box3d_tbk_sep_kernel(T* __restrict__ out,
+                                                          const __grid_constant__ CUtensorMap tmap,
+                                                          const __grid_constant__ BoxArgs<T> a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int SLOT = slot_bytes<T>() / (int)sizeof(T);
+    constexpr int BE = b_bytes<T>() / (int)sizeof(T);
+    constexpr int BX = BXW<T>, PL = PAD<T>, BW = BWP<T>;
+    constexpr int HX = HXK<KL, T>, TX = TXK<KL, T>, TY = TYK<KL>;
+    T* ring = reinterpret_cast<T*>(smem);
+    T* buf = reinterpret_cast<T*>(smem + STAGES * slot_bytes<T>());
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * slot_bytes<T>() +
+                                                (KL - 1) * NB * b_bytes<T>());
+
+    const int tid = threadIdx.x;
+    const int lx = tid % NLX, ly = tid / NLX;
+    const int tile = blockIdx.x;
+    const int bx = tile % a.tiles_x;
+    const int by = (tile / a.tiles_x) % a.tiles_y;
+    const int bz = tile / (a.tiles_x * a.tiles_y);
+    const int gx = bx * TX - HX, gy = by * TY - (KL - 1);  // global coords of region cell (0, 0)
+    const int i0 = a.lo0 + bz * a.chunk;
+    const int i1 = min(i0 + a.chunk, a.hi0);
+    constexpr int LAG = 2 * KL - 1;  // output plane = ring plane - LAG
+    const int t_begin = i0 - KL, niter = i1 - i0 + LAG + KL;
+    const int x = VX * lx, y = VY * ly;
+
+    bool cint[VY][VX], cout[VY][VX];
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) {
+            const int ga1 = gy + y + cy, ga2 = gx + x + cx;
+            cint[cy][cx] = ga1 >= 0 && ga1 < a.n1 && ga2 >= 0 && ga2 < a.n2;
+            cout[cy][cx] = cint[cy][cx] && y + cy >= KL - 1 && y + cy < L1Y - (KL - 1) &&
+                           x + cx >= HX && x + cx < HX + TX;
+        }
+    bool mine = true;
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) mine &= cint[cy][cx];
+    const bool warp_int = __all_sync(0xffffffffu, mine);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&tmap);
+    }
+    __syncthreads();
+    constexpr unsigned kBoxBytes = BX * BY * sizeof(T);
+    const int c0 = a.off2 + gx - PL, c1 = a.h1 + gy - 1;
+    // level-0 planes of the dependency cone are [i0-KL, i1+KL); the drain
+    // steps re-load the last one, so a launch never reads outside its cone
+    // (a slab's interior range runs while its ghost planes are written)
+    const int last_plane = a.h0 + i1 + KL - 1;
+    if (tid == 0)
+        for (int s = 0; s < STAGES && s < niter; ++s) {
+            mbar_expect_tx(&bar[s], kBoxBytes);
+            tma_load_3d(ring + s * SLOT, &tmap, &bar[s], c0, c1, min(a.h0 + t_begin + s, last_plane));
+        }
+
+    T accA[KL][VY][VX], accB[KL][VY][VX];  // per level: outputs p+1 (started), p (open)
+    T keep0[VY][VX];  // level-0 centre of the previous ring plane (Dirichlet cells of level 1)
+#pragma unroll
+    for (int l = 0; l < KL; ++l)
+#pragma unroll
+        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < VX; ++cx) accA[l][cy][cx] = accB[l][cy][cx] = T(0);
+#pragma unroll
+    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < VX; ++cx) keep0[cy][cx] = T(0);
+    const T w = a.w[0];
+    using V4 = typename VecT<T, 16 / sizeof(T)>::type;
+    constexpr int NV = 16 / sizeof(T);
+
+    T* orow = out + (a.origin + (long long)(t_begin - LAG) * a.pitch0 +
+                     (long long)(gy + y) * a.pitch1 + (gx + x));
+    for (int it = 0; it < niter; ++it, orow += a.pitch0) {
+        const int q = t_begin + it;  // level-0 plane in the ring
+        const int slot = it % STAGES;
+        mbar_wait(&bar[slot], (it / STAGES) & 1);
+        // level l consumes the level-(l-1) plane c_l = q - 2(l-1) and
+        // finishes output plane c_l - 1; levels in descending order so each
+        // reads its source buffer before the level below republishes
+#pragma unroll
+        for (int l = KL; l >= 1; --l) {
+            const int c = q - 2 * (l - 1);  // consumed level-(l-1) plane
+            T nb[VY + 2][VX + 2];
+            if (l == 1) {
+#pragma unroll
+                for (int r = 0; r < VY + 2; ++r)
+                    load_row<T, NLX>(ring + slot * SLOT + PL + x + (y + r) * BX, x, lx, nb[r]);
+            } else {
+                const T* B = buf + ((l - 2) * NB + ((c % NB) + NB) % NB) * BE;
+#pragma unroll
+                for (int r = 0; r < VY + 2; ++r)
+                    load_row<T, NLX>(B + PL + x + (y + r) * BW, x, lx, nb[r]);
+            }
+            T ps[VY][VX];
+            plane_sum9(nb, ps);
+            T v[VY][VX];  // level-l plane c-1
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) {
-                    a2B[cy][cx] = a2A[cy][cx] + ps2[cy][cx];
-                    a2A[cy][cx] = ps2[cy][cx];
+                    v[cy][cx] = w * (accB[l - 1][cy][cx] + ps[cy][cx]);
+                    accB[l - 1][cy][cx] = accA[l - 1][cy][cx] + ps[cy][cx];
+                    accA[l - 1][cy][cx] = ps[cy][cx];
                 }
-        } else {
-            apply9<EXACT, false, T, Q>(a.w + 9, nb2, a2A);
+            const int p = c - 1;
+            if (l < KL) {
+                // Dirichlet: cells outside the interior keep their level-0 value
+                // (value of level l-1 at plane p: for l = 1 the previous ring
+                // plane's centre kept in registers; for l > 1 the level-(l-1)
+                // plane p still in its SMEM slot — level l-1 overwrites it only
+                // later in this step)
+                if (!(warp_int && p >= 0 && p < a.n0)) {  // warp-uniform
+                    const bool pint = p >= 0 && p < a.n0;
+                    T kv[VY][VX];
+                    if (l == 1) {
 #pragma unroll
-            for (int cy = 0; cy < VY; ++cy)
+                        for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-                for (int cx = 0; cx < VX; ++cx) a2B[cy][cx] = a2A[cy][cx];
-            apply9<EXACT, true, T, Q>(a.w, nb2, a2A);
+                            for (int cx = 0; cx < VX; ++cx) kv[cy][cx] = keep0[cy][cx];
+                    } else {
+                        const T* Bp = buf + ((l - 2) * NB + ((p % NB) + NB) % NB) * BE;
+#pragma unroll
+                        for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                            for (int cx = 0; cx < VX; ++cx)
+                                kv[cy][cx] = Bp[(y + cy + 1) * BW + x + PL + cx];
+                    }
+#pragma unroll
+                    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                        for (int cx = 0; cx < VX; ++cx)
+                            if (!(pint && cint[cy][cx])) v[cy][cx] = kv[cy][cx];
+                }
+                if (l == 1 && (!warp_int || c - 1 < 0 || c + 1 >= a.n0)) {  // next plane may select
+#pragma unroll
+                    for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                        for (int cx = 0; cx < VX; ++cx) keep0[cy][cx] = nb[cy + 1][cx + 1];
+                }
+                T* B = buf + ((l - 1) * NB + ((p % NB) + NB) % NB) * BE;
+#pragma unroll
+                for (int cy = 0; cy < VY; ++cy)
+#pragma unroll
+                    for (int vv = 0; vv < VX; vv += NV) {
+                        V4 o;
+                        T* e = reinterpret_cast<T*>(&o);
+#pragma unroll
+                        for (int u = 0; u < NV; ++u) e[u] = v[cy][vv + u];
+                        *reinterpret_cast<V4*>(B + (y + cy + 1) * BW + x + PL + vv) = o;
+                    }
+            } else if (p >= i0 && p < i1) {  // p = q - LAG
+#pragma unroll
+                for (int cy = 0; cy < VY; ++cy) {
+                    store_row<T, VX>(orow + cy * a.pitch1, v[cy], cout[cy]);
+                    if (a.mirror)
+                        store_row<T, VX>(a.mirror + (orow - out) + a.mshift + cy * a.pitch1, v[cy],
+                                         cout[cy]);
+                }
+            }
+        }
+        __syncthreads();  // level planes published; ring slot of plane q free
+        if (tid == 0 && it + STAGES < niter) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[slot], kBoxBytes);
+            tma_load_3d(ring + slot * SLOT, &tmap, &bar[slot], c0, c1,
+                        min(a.h0 + t_begin + it + STAGES, last_plane));
         }
     }
 }
@@ -542,7 +703,10 @@ bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused)
 
 // FAST with uniform weights runs the separable sums (8 operations per
 // update): k = 2 halves the HBM traffic per step (C4: 714 -> 799 GS/s).
+// (k = 3 / 4 run the same pipeline with 199 / 250 registers: 867 / 728
+// GS/s on C4 against 1060 at k = 2, so 2 is the default.)
 int fast_default(const TapSet& t) { return uniform_weights(t) ? 2 : 1; }
+int fast_max(const TapSet& t) { return uniform_weights(t) ? 4 : 2; }
 
 template <typename T, int MODE>
 Status launch(const LaunchCtx& c, const void* in, void* out) {
@@ -620,16 +784,58 @@ Status launch2(const LaunchCtx& c, const void* in, void* out) {
     return Status::Ok();
 }
 
+template <typename T, int KL>
+Status launchk(const LaunchCtx& c, const void* in, void* out) {
+    const Geo& g = *c.g;
+    CUtensorMap map;
+    Status s = make_tmap_3d<T>(g, in, BXW<T>, BY, &map);
+    if (!s.ok()) return s;
+    BoxArgs<T> a;
+    a.n0 = (int)g.n[0];
+    a.n1 = (int)g.n[1];
+    a.n2 = (int)g.n[2];
+    a.tiles_x = (int)((g.n[2] + TXK<KL, T> - 1) / TXK<KL, T>);
+    a.tiles_y = (int)((g.n[1] + TYK<KL> - 1) / TYK<KL>);
+    a.h0 = (int)g.h[0];
+    a.h1 = (int)g.h[1];
+    a.off2 = (int)g.off2;
+    a.pitch0 = g.pitch[0];
+    a.pitch1 = g.pitch[1];
+    a.origin = g.origin;
+    a.mirror = static_cast<T*>(c.mirror);
+    a.mshift = c.mirror_shift;
+    for (int q = 0; q < 27; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
+    constexpr int bytes = smemk_bytes<KL, T>();
+    int per_sm = 1, nsm = 148;
+    s = occupancy(box3d_tbk_sep_kernel<T, KL>, NT, bytes, &per_sm, &nsm);
+    if (!s.ok()) return s;
+    const long long tiles = (long long)a.tiles_x * a.tiles_y;
+    a.lo0 = (int)c.range_lo();
+    a.hi0 = (int)c.range_hi();
+    if (a.hi0 <= a.lo0) return Status::Ok();
+    const int64_t span = a.hi0 - a.lo0;
+    a.chunk = pick_chunk(span, tiles, (long long)nsm * per_sm, 3 * KL, 32);
+    const long long nchunks = (span + a.chunk - 1) / a.chunk;
+    box3d_tbk_sep_kernel<T, KL><<<(unsigned)(tiles * nchunks), NT, bytes, c.stream>>>(
+        static_cast<T*>(out), map, a);
+    TSR_CUDA_TRY(cudaGetLastError());
+    return Status::Ok();
+}
+
 template <typename T>
 Status run_t(const LaunchCtx& c, const void* in, void* out, int k) {
     // uniform weights: Q in EXACT mode (bitwise), separable sums in FAST
     const int mode = uniform_weights(*c.taps) ? (c.exact ? 2 : 3) : c.exact ? 1 : 0;
+    if (mode == 3 && k >= 2) {  // SEP: the k-level skewed pipeline
+        if (k == 3) return launchk<T, 3>(c, in, out);
+        if (k == 4) return launchk<T, 4>(c, in, out);
+        return launchk<T, 2>(c, in, out);
+    }
     if (k == 2) {
         switch (mode) {
             case 0: return launch2<T, 0>(c, in, out);
             case 1: return launch2<T, 1>(c, in, out);
-            case 2: return launch2<T, 2>(c, in, out);
-            default: return launch2<T, 3>(c, in, out);
+            default: return launch2<T, 2>(c, in, out);
         }
     }
     if (k != 1) return Status::Err(TSR_EUNSUPPORTED, "box3d fuses one or two steps per pass");
@@ -648,6 +854,6 @@ Status run(const LaunchCtx& c, const void* in, void* out, int k) {
 
 }  // namespace
 
-extern const Engine kBox3dEngine = {"box3d_r1_planesum", supports, run, fast_default};
+extern const Engine kBox3dEngine = {"box3d_r1_planesum", supports, run, fast_default, fast_max};
 
 }  // namespace tsr

@@ -495,3 +495,24 @@ def test_staged_transfers_halo_and_cache_sizes(ts, orc):
     with pytest.raises(ValueError, match="halo"):
         ts.run_gpu(g, k, 3)
     assert [g.buffer(w).tobytes() for w in (0, 1)] == before and g.parity == 0
+
+
+@pytest.mark.parametrize("fused", [2, 3, 4])
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_box27_separable_fast_within_tolerance(ts, orc, dt, fused):
+    """box3d FAST mode for the uniform 27-point box: the k-level skewed
+    pipeline of separable sums, ragged tiles, chunked a0, a non-zero halo
+    plane, within the north star's tolerance of the oracle (max-rel and
+    L2-rel)."""
+    k = ts.find_benchmark("Box-3D27P").kernel
+    for extent in ([40, 37, 70], [21, 64, 131], [9, 10, 11], [70, 45, 150]):
+        a = random_grid(ts, orc, extent, [1, 1, 1], 3, dt)
+        a.padded(0)[0] = 2.5
+        a.padded(1)[0] = 2.5
+        b = a.copy()
+        st = ts.run_gpu(a, k, 13, fused_steps=fused, mode="fast")
+        orc.naive_run(b, k, 13)
+        assert st.fused_steps == fused
+        d = ts.deviation(a, b)
+        assert d["max_rel_deviation"] <= TOL[dt] and d["l2_rel_err"] <= TOL[dt], (extent, d)
+        assert halos_equal(a, b)
