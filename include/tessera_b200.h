@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TSR_ABI_VERSION 2
+#define TSR_ABI_VERSION 3
 
 enum tsr_status {
     TSR_OK = 0,
@@ -261,6 +261,11 @@ typedef struct tsr_comm_record {
     int32_t from_slab, to_slab;
     int64_t bytes;         /* depth * interior cross-section * sizeof(T)     */
     double seam_ms;        /* device time of the sender's seam passes        */
+    /* Timeline of the sender's round on its device, ms after the first
+     * logged round of that slab: seam passes [seam_t0, seam_t1) on the seam
+     * stream, interior pass [interior_t0, interior_t1) on the second stream
+     * (equal when the slab has no interior planes). */
+    double seam_t0_ms, seam_t1_ms, interior_t0_ms, interior_t1_ms;
 } tsr_comm_record;
 
 /* Validates the partition (each slab >= r*k planes, the reference's

@@ -32,7 +32,7 @@ EXPORTED = (
     "tsr_multi_advance", "tsr_multi_download", "tsr_multi_slab_info", "tsr_multi_set_logging",
     "tsr_multi_comm_log", "tsr_multi_plane_checksums", "tsr_plane_checksums", "tsr_run_multi",
 )
-ABI_VERSION = 2
+ABI_VERSION = 3
 TSR_XPORT_AUTO, TSR_XPORT_MIRROR, TSR_XPORT_COPY = 0, 1, 2
 TRANSPORTS = {"auto": TSR_XPORT_AUTO, "mirror": TSR_XPORT_MIRROR, "copy": TSR_XPORT_COPY}
 TSR_PART_POISON = 1
@@ -109,6 +109,10 @@ class TsrCommRecord(ctypes.Structure):
         ("to_slab", ctypes.c_int32),
         ("bytes", ctypes.c_int64),
         ("seam_ms", ctypes.c_double),
+        ("seam_t0_ms", ctypes.c_double),
+        ("seam_t1_ms", ctypes.c_double),
+        ("interior_t0_ms", ctypes.c_double),
+        ("interior_t1_ms", ctypes.c_double),
     ]
 
 

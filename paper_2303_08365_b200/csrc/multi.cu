@@ -55,7 +55,8 @@ struct Slab {
 struct LogEntry {
     int64_t round;
     int slab;
-    cudaEvent_t a, b;
+    cudaEvent_t a, b;  // seam passes (seam stream)
+    cudaEvent_t c, d;  // interior pass (second stream)
 };
 
 }  // namespace
@@ -125,11 +126,15 @@ void free_slab(Slab& sl) {
 }
 
 void drop_log(Multi& m) {
+    int prev = 0;
+    cudaGetDevice(&prev);
     for (LogEntry& e : m.log) {
-        cudaEventDestroy(e.a);
-        cudaEventDestroy(e.b);
+        cudaSetDevice(m.s[e.slab].device);
+        for (cudaEvent_t ev : {e.a, e.b, e.c, e.d})
+            if (ev) cudaEventDestroy(ev);
     }
     m.log.clear();
+    cudaSetDevice(prev);
 }
 
 void destroy(Multi* m) {
@@ -516,10 +521,10 @@ Status run_round(Multi& m, int n, tsr_stats& st) {
                     TSR_CUDA_TRY(cudaStreamWaitEvent(sl.s_seam,
                                                      m.s[sl.nb[side]].ev_seam[(rnd - 1) & 1], 0));
         }
-        LogEntry le{rnd, static_cast<int>(i), nullptr, nullptr};
+        LogEntry le{rnd, static_cast<int>(i), nullptr, nullptr, nullptr, nullptr};
         if (m.logging) {
-            TSR_CUDA_TRY(cudaEventCreate(&le.a));
-            TSR_CUDA_TRY(cudaEventCreate(&le.b));
+            for (cudaEvent_t* ev : {&le.a, &le.b, &le.c, &le.d})
+                TSR_CUDA_TRY(cudaEventCreate(ev));
             TSR_CUDA_TRY(cudaEventRecord(le.a, sl.s_seam));
         }
         const int64_t first = sl.ghost_lo, last = sl.ghost_lo + sl.own();
@@ -552,20 +557,22 @@ Status run_round(Multi& m, int n, tsr_stats& st) {
             st.ghost_recompute_points += rad * (kk * n - int64_t(n) * (n + 1) / 2) * m.cross;
         }
         TSR_CUDA_TRY(cudaEventRecord(sl.ev_seam[rnd & 1], sl.s_seam));
-        if (m.logging) {
-            TSR_CUDA_TRY(cudaEventRecord(le.b, sl.s_seam));
-            m.log.push_back(le);
-        }
+        if (m.logging) TSR_CUDA_TRY(cudaEventRecord(le.b, sl.s_seam));
         // ---- interior stream: planes whose n-step cone stays inside the
         // owned planes; concurrent with the seam passes
         if (rnd > 0)
             TSR_CUDA_TRY(cudaStreamWaitEvent(sl.s_int, sl.ev_seam[(rnd - 1) & 1], 0));
         const int64_t ilo = first + (sl.nb[0] >= 0 ? m.depth : 0);
         const int64_t ihi = last - (sl.nb[1] >= 0 ? m.depth : 0);
+        if (m.logging) TSR_CUDA_TRY(cudaEventRecord(le.c, sl.s_int));
         if (ihi > ilo) {
             Status r = sweep_range(m, sl, sl.s_int, ilo, ihi, n, nullptr, 0);
             if (!r.ok()) return r;
             ++st.kernel_launches;
+        }
+        if (m.logging) {
+            TSR_CUDA_TRY(cudaEventRecord(le.d, sl.s_int));
+            m.log.push_back(le);
         }
         TSR_CUDA_TRY(cudaEventRecord(sl.ev_int, sl.s_int));
     }
@@ -891,13 +898,22 @@ int tsr_multi_comm_log(tsr_multi* m, tsr_comm_record* out, int64_t cap, int64_t*
     if (!r.ok()) return report(r);
     int64_t n = 0;
     const int64_t bytes = m->depth * m->cross * m->g.esize;
+    std::vector<cudaEvent_t> epoch(m->s.size(), nullptr);  // per slab: its first logged round
+    for (const LogEntry& e : m->log)
+        if (!epoch[e.slab]) epoch[e.slab] = e.a;
     for (const LogEntry& e : m->log) {
-        float ms = 0.f;
+        cudaSetDevice(m->s[e.slab].device);
+        float ms = 0.f, s0 = 0.f, s1 = 0.f, i0 = 0.f, i1 = 0.f;
         cudaEventElapsedTime(&ms, e.a, e.b);
+        cudaEventElapsedTime(&s0, epoch[e.slab], e.a);
+        cudaEventElapsedTime(&s1, epoch[e.slab], e.b);
+        cudaEventElapsedTime(&i0, epoch[e.slab], e.c);
+        cudaEventElapsedTime(&i1, epoch[e.slab], e.d);
         const Slab& sl = m->s[e.slab];
         for (int side = 0; side < 2; ++side) {
             if (sl.nb[side] < 0) continue;
-            if (out && n < cap) out[n] = tsr_comm_record{e.round, e.slab, sl.nb[side], bytes, ms};
+            if (out && n < cap)
+                out[n] = tsr_comm_record{e.round, e.slab, sl.nb[side], bytes, ms, s0, s1, i0, i1};
             ++n;
         }
     }

@@ -310,18 +310,41 @@ class SlabGrid:
     def set_logging(self, on: bool = True) -> None:
         _abi.check(_abi.lib().tsr_multi_set_logging(self._h, int(bool(on))))
 
-    def comm_records(self, model: CommCostModel | None = None) -> list:
-        """CommRecords of the rounds run since logging was switched on (or
-        since the last call); direction "w{from}_to_w{to}" as the reference
-        names its two workers' messages."""
-        model = model or CommCostModel()
+    def _raw_log(self) -> list:
+        """The runtime's delivery records since logging was switched on (or
+        since the last read), consumed (tsr_multi_comm_log)."""
         L = _abi.lib()
         n = ctypes.c_int64()
         _abi.check(L.tsr_multi_comm_log(self._h, None, 0, ctypes.byref(n)))
         arr = (_abi.TsrCommRecord * max(1, n.value))()
         _abi.check(L.tsr_multi_comm_log(self._h, arr, n.value, ctypes.byref(n)))
+        return list(arr[:n.value])
+
+    def round_timeline(self) -> list:
+        """Per slab and round, on the slab's device (ms after its first
+        logged round): the seam passes' interval on the seam stream and the
+        interior pass's on the second stream — the overlap of exchange and
+        compute that the reference gets from its worker threads
+        (HaloWorker::run_round, scheduler.cpp:371-406).  Consumes the log."""
+        seen, out = set(), []
+        for r in self._raw_log():
+            key = (int(r.round), int(r.from_slab))
+            if key in seen:
+                continue
+            seen.add(key)
+            out.append({"round": key[0], "slab": key[1],
+                        "seam": [r.seam_t0_ms, r.seam_t1_ms],
+                        "interior": [r.interior_t0_ms, r.interior_t1_ms]})
+        out.sort(key=lambda e: (e["round"], e["slab"]))
+        return out
+
+    def comm_records(self, model: CommCostModel | None = None) -> list:
+        """CommRecords of the rounds run since logging was switched on (or
+        since the last call); direction "w{from}_to_w{to}" as the reference
+        names its two workers' messages."""
+        model = model or CommCostModel()
         out = []
-        for r in arr[:n.value]:
+        for r in self._raw_log():
             out.append(CommRecord(int(r.round), f"w{r.from_slab}_to_w{r.to_slab}", int(r.bytes),
                                   model.alpha + float(r.bytes) * model.beta, r.seam_ms / 1e3))
         out.sort(key=lambda r: (r.round, r.direction))

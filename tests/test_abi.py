@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol(ts):
     for name in syms:
         assert hasattr(L, name), name
     assert set(syms) == set(_abi.EXPORTED)
-    assert L.tsr_abi_version() == _abi.ABI_VERSION == 2
+    assert L.tsr_abi_version() == _abi.ABI_VERSION == 3
 
 
 def test_library_is_sm100a(ts):

@@ -331,3 +331,23 @@ def test_run_gpu_ngpus_and_errors(ts, orc):
                      devices=_devices(4), fused_steps=3)
     with pytest.raises(ValueError, match="boundary outside"):
         ts.run_multi(g, k, 2, 2, devices=_devices(2), boundaries=[40])
+
+
+@pytest.mark.gpu
+def test_round_timeline_shows_concurrent_seam_and_interior(ts):
+    """Per round and slab the runtime logs the seam passes' interval (seam
+    stream) and the interior pass's (second stream); the interior pass of a
+    round is issued without waiting for that round's seam passes, so the
+    two intervals of a slab overlap in time."""
+    k = ts.find_benchmark("Heat-3D").kernel
+    with ts.SlabGrid(k, [192, 64, 64], ngpus=2, devices=_devices(2), fused_steps=3,
+                     mode="fast") as sg:
+        sg.fill_random(1)
+        sg.set_logging(True)
+        st = sg.advance(18)
+        tl = sg.round_timeline()
+    assert len(tl) == 2 * 6 and st.rounds == 6
+    for e in tl:
+        assert e["seam"][0] <= e["seam"][1] and e["interior"][0] <= e["interior"][1]
+    assert any(min(e["seam"][1], e["interior"][1]) > max(e["seam"][0], e["interior"][0])
+               for e in tl)
