@@ -1,8 +1,10 @@
 """One small run of every CUDA engine, for compute-sanitizer (memcheck,
-racecheck, synccheck): tb3d k=1..3 (TMA ring + mbarriers), box3d k=1..2,
-stream2d (cp.async ring), stream1d, the generic engine, the mirrored seam
-pass of a two-slab round, each checked bitwise against the oracle so a
-sanitizer-visible race that changed results would also fail here.
+racecheck, synccheck): tb3d k=1..3 (TMA ring + mbarriers), box3d k=1..2 and
+its separable k-level pipeline, stream2d (cp.async ring; Q and separable
+modes), stream1d, the generic engine, the mirrored seam pass of a two-slab
+round, each checked against the oracle (bitwise, or within tolerance for the
+FAST separable modes) so a sanitizer-visible race that changed results would
+also fail here.
 
     compute-sanitizer --tool racecheck python tools/sanitize_engines.py
 """
@@ -43,6 +45,22 @@ def main():
         ok = g.interior_view(g.parity).tobytes() == ref.interior_view(ref.parity).tobytes()
         print(f"{name} {ext} {dt} T={steps} k={st.fused_steps} engine={st.engine}: "
               f"{'bitwise ok' if ok else 'MISMATCH'}", flush=True)
+        assert ok
+    # FAST-mode separable box kernels (stream2d SEP, box3d k-level pipeline),
+    # within the tolerance of the oracle
+    for name, ext, steps, fused, dt in [("Box-2D9P", [70, 300], 8, 4, "f64"),
+                                        ("Box-3D27P", [14, 20, 70], 5, 2, "f32"),
+                                        ("Box-3D27P", [14, 20, 70], 6, 3, "f64")]:
+        k = ts.find_benchmark(name).kernel
+        g = (ts.Grid if dt == "f64" else ts.GridF)(ext, [k.radius] * k.dims)
+        ts.fill_random(g, 6)
+        ref = g.copy()
+        st = ts.run_gpu(g, k, steps, fused_steps=fused, mode="fast")
+        orc.naive_run(ref, k, steps)
+        d = ts.deviation(g, ref)["max_rel_deviation"]
+        ok = d <= (1e-12 if dt == "f64" else 1e-5)
+        print(f"{name} {ext} {dt} T={steps} k={st.fused_steps} fast: max_rel {d:.2e} "
+              f"{'ok' if ok else 'OUT OF TOLERANCE'}", flush=True)
         assert ok
     for name, ext, steps, dt in GENERIC:
         k = ts.find_benchmark(name).kernel
