@@ -351,3 +351,24 @@ def test_round_timeline_shows_concurrent_seam_and_interior(ts):
         assert e["seam"][0] <= e["seam"][1] and e["interior"][0] <= e["interior"][1]
     assert any(min(e["seam"][1], e["interior"][1]) > max(e["seam"][0], e["interior"][0])
                for e in tl)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,extent,dt,fused,P", [
+    ("Box-3D27P", [60, 30, 70], "f32", 2, 2),   # C4's bench path: separable k-level pipeline
+    ("Box-3D27P", [61, 30, 70], "f32", 3, 3),
+    ("Box-2D9P", [130, 150], "f64", 4, 3),      # stream2d separable mode
+    ("Heat-3D", [70, 40, 66], "f64", 3, 4),
+])
+def test_slabs_fast_equal_one_device_fast(ts, orc, name, extent, dt, fused, P):
+    """FAST-mode slab runs (seam passes with mirror stores + interior
+    ranges) are bitwise the same FAST run on one device: every engine's range
+    and mirror path computes each point exactly as its full pass does."""
+    k = bench_kernel(ts, name)
+    g = random_grid(ts, orc, extent, [1] * k.dims, 77, dt)
+    one = g.copy()
+    ts.run_multi(g, k, 11, P, devices=_devices(P), fused_steps=fused, mode="fast")
+    ts.run_gpu(one, k, 11, fused_steps=fused, mode="fast")
+    assert g.parity == one.parity
+    for w in (0, 1):
+        assert g.interior_view(w).tobytes() == one.interior_view(w).tobytes(), w
