@@ -590,8 +590,10 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
         if (tiles >= slots) {  // phase 1: whole tiles, aligned planes
             grid = (unsigned)slots;
             a.full_tiles = (int)(tiles / slots);
-            const long long rest = (tiles - (long long)a.full_tiles * slots) * span;
-            a.per_cta = (rest + slots - 1) / slots;
+            const long long left = tiles - (long long)a.full_tiles * slots;
+            // nearly one leftover tile per CTA (C5: 132 for 148): whole tiles,
+            // aligned, a few SMs idle; otherwise an even split of the planes
+            a.per_cta = left * 100 >= slots * 85 ? span : (left * span + slots - 1) / slots;
         } else if (tiles * 10 >= slots * 9) {
             // nearly one tile per SM (C3: 144 tiles, 148 SMs): one whole tile
             // per CTA keeps the planes aligned; an even split would leave 4
