@@ -252,8 +252,8 @@ Status plan_for(const Geo& g, const TapSet& t, const tsr_opts& o, Plan& p) {
     if (!e) {
         p.k = 1;
     } else {
-        if (o.mode == TSR_FAST && e->fast_max) maxk = e->fast_max(t);
-        if (o.mode == TSR_FAST && e->fast_default) defk = std::min(e->fast_default(t), maxk);
+        if (o.mode == TSR_FAST && e->fast_max) maxk = e->fast_max(g, t);
+        if (o.mode == TSR_FAST && e->fast_default) defk = std::min(e->fast_default(g, t), maxk);
         p.k = o.fused_steps > 0 ? std::min(o.fused_steps, maxk) : defk;
     }
     return Status::Ok();

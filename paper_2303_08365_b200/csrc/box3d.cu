@@ -701,12 +701,15 @@ bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused)
     return true;
 }
 
-// FAST with uniform weights runs the separable sums (8 operations per
-// update): k = 2 halves the HBM traffic per step (C4: 714 -> 799 GS/s).
-// (k = 3 / 4 run the same pipeline with 199 / 250 registers: 867 / 728
-// GS/s on C4 against 1060 at k = 2, so 2 is the default.)
-int fast_default(const TapSet& t) { return uniform_weights(t) ? 2 : 1; }
-int fast_max(const TapSet& t) { return uniform_weights(t) ? 4 : 2; }
+// FAST with uniform weights runs the separable sums: fp32 in tbbox.cu
+// (register windows of plane sums, k = 3 default: C4 1238 GS/s, against
+// 1068 at k = 2 and 714 for EXACT's Q mode), fp64 in the k-level
+// shared-memory pipeline above (k = 2: 199 / 250 registers at k = 3 / 4).
+int fast_default(const Geo& g, const TapSet& t) {
+    if (!uniform_weights(t)) return 1;
+    return g.dtype == TSR_F32 ? 3 : 2;
+}
+int fast_max(const Geo&, const TapSet& t) { return uniform_weights(t) ? 4 : 2; }
 
 template <typename T, int MODE>
 Status launch(const LaunchCtx& c, const void* in, void* out) {
@@ -822,10 +825,13 @@ Status launchk(const LaunchCtx& c, const void* in, void* out) {
     return Status::Ok();
 }
 
+Status tbbox_run_dispatch(const LaunchCtx& c, const void* in, void* out, int k);
+
 template <typename T>
 Status run_t(const LaunchCtx& c, const void* in, void* out, int k) {
     // uniform weights: Q in EXACT mode (bitwise), separable sums in FAST
     const int mode = uniform_weights(*c.taps) ? (c.exact ? 2 : 3) : c.exact ? 1 : 0;
+    if (mode == 3 && sizeof(T) == 4) return tbbox_run_dispatch(c, in, out, k);
     if (mode == 3 && k >= 2) {  // SEP: the k-level skewed pipeline
         if (k == 3) return launchk<T, 3>(c, in, out);
         if (k == 4) return launchk<T, 4>(c, in, out);
@@ -852,6 +858,14 @@ Status run(const LaunchCtx& c, const void* in, void* out, int k) {
     return run_t<float>(c, in, out, k);
 }
 
+}  // namespace
+
+Status tbbox_run(const LaunchCtx& c, const void* in, void* out, int k);
+
+namespace {
+Status tbbox_run_dispatch(const LaunchCtx& c, const void* in, void* out, int k) {
+    return tbbox_run(c, in, out, k);
+}
 }  // namespace
 
 extern const Engine kBox3dEngine = {"box3d_r1_planesum", supports, run, fast_default, fast_max};

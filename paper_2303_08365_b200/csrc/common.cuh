@@ -211,9 +211,9 @@ struct Engine {
     Status (*run)(const LaunchCtx&, const void* in, void* out, int k);
     // Optional: the default fused depth in FAST mode when it differs from
     // the EXACT one (nullptr = same as supports()'s default_fused).
-    int (*fast_default)(const TapSet&) = nullptr;
+    int (*fast_default)(const Geo&, const TapSet&) = nullptr;
     // Optional: the largest fused depth in FAST mode when it differs.
-    int (*fast_max)(const TapSet&) = nullptr;
+    int (*fast_max)(const Geo&, const TapSet&) = nullptr;
 };
 const Engine* find_engine(const Geo& g, const TapSet& t, int* max_fused, int* default_fused);
 

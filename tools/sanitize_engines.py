@@ -50,7 +50,8 @@ def main():
     # within the tolerance of the oracle
     for name, ext, steps, fused, dt in [("Box-2D9P", [70, 300], 8, 4, "f64"),
                                         ("Box-3D27P", [14, 20, 70], 5, 2, "f32"),
-                                        ("Box-3D27P", [14, 20, 70], 6, 3, "f64")]:
+                                        ("Box-3D27P", [14, 20, 70], 6, 3, "f64"),
+                                        ("Box-3D27P", [14, 30, 300], 9, 3, "f32")]:
         k = ts.find_benchmark(name).kernel
         g = (ts.Grid if dt == "f64" else ts.GridF)(ext, [k.radius] * k.dims)
         ts.fill_random(g, 6)
