@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(NT1<T>) box3d_kernel(T* __restrict__ out,
 #pragma unroll
             for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
-                for (int cx = 0; cx < VX; ++cx) accB[cy][cx] = a.w[0] * (accB[cy][cx] + ps[cy][cx]);
+                for (int cx = 0; cx < VX; ++cx) accB[cy][cx] = mul_rn(a.w[0], accB[cy][cx] + ps[cy][cx]);
         } else {
             // finish output q-1 (di = +1 taps)
             apply9<EXACT, false, T, Q>(a.w + 18, nb, accB);
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(NT) box3d_tbk_sep_kernel(T* __restrict__ out,
             for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
                 for (int cx = 0; cx < VX; ++cx) {
-                    v[cy][cx] = w * (accB[l - 1][cy][cx] + ps[cy][cx]);
+                    v[cy][cx] = mul_rn(w, accB[l - 1][cy][cx] + ps[cy][cx]);
                     accB[l - 1][cy][cx] = accA[l - 1][cy][cx] + ps[cy][cx];
                     accA[l - 1][cy][cx] = ps[cy][cx];
                 }

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) stream2d_kernel(
             for (int v = 0; v < V; ++v) {
                 if constexpr (SEP) {
                     const int sm = (sx + P - 1) % P, sp = (sx + 1) % P;
-                    T nv = a.w[0] * ((hwin[l - 1][sm][v] + hwin[l - 1][sx][v]) + hwin[l - 1][sp][v]);
+                    T nv = mul_rn(a.w[0], (hwin[l - 1][sm][v] + hwin[l - 1][sx][v]) + hwin[l - 1][sp][v]);
                     if constexpr (SEL) {
                         const bool rint = x >= 0 && x < a.rows;
                         if (l < K) nv = (rint && cint[v]) ? nv : win[l - 1][sx][R + v];

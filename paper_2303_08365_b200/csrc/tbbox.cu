@@ -9,7 +9,11 @@
 // so each level keeps two open accumulators per point (accB = P(p-1)+P(p),
 // accA = P(p+1)) and consumes one source plane per step.  Within the
 // north star's tolerance of the oracle's lexicographic order (1e-5 fp32;
-// only the rounding of the reassociated sum differs).
+// only the rounding of the reassociated sum differs).  The weight multiply is
+// __fmul_rn: were it left to the compiler, it could be contracted into an FMA
+// with the next level's h additions in some step tiers and not others, and a
+// point's bits would depend on the tiling (a slab run would not reproduce a
+// one-device run).
 //
 //  * Memory tier: a CTA owns a 128 (a2) x R1Y (a1) level-1 region and
 //    streams a0 planes of it; level-0 planes (region + 1-cell halo) arrive
@@ -186,7 +190,7 @@ __device__ __forceinline__ void box_step(const BoxArgs& a, T* __restrict__ out, 
         for (int cy = 0; cy < VY; ++cy)
 #pragma unroll
             for (int v = 0; v < VX; ++v) {
-                res[cy][v] = a.w * (accB[l - 1][cy][v] + ps[cy][v]);
+                res[cy][v] = __fmul_rn(a.w, accB[l - 1][cy][v] + ps[cy][v]);
                 accB[l - 1][cy][v] = acc[l - 1][PH ^ 1][cy][v] + ps[cy][v];
             }
         if (l < K) {

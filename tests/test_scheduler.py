@@ -359,6 +359,11 @@ def test_round_timeline_shows_concurrent_seam_and_interior(ts):
     ("Box-3D27P", [61, 30, 70], "f32", 3, 3),
     ("Box-2D9P", [130, 150], "f64", 4, 3),      # stream2d separable mode
     ("Heat-3D", [70, 40, 66], "f64", 3, 4),
+    # several tiles per axis and several segments per CTA: step tiers differ
+    # between the slab and one-device runs, the bits may not (a contracted
+    # FMA in one tier once made them differ)
+    ("Box-3D27P", [40, 256, 1024], "f32", 3, 2),
+    ("Box-2D9P", [700, 2000], "f64", 4, 3),
 ])
 def test_slabs_fast_equal_one_device_fast(ts, orc, name, extent, dt, fused, P):
     """FAST-mode slab runs (seam passes with mirror stores + interior
