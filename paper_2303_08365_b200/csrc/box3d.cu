@@ -831,7 +831,8 @@ template <typename T>
 Status run_t(const LaunchCtx& c, const void* in, void* out, int k) {
     // uniform weights: Q in EXACT mode (bitwise), separable sums in FAST
     const int mode = uniform_weights(*c.taps) ? (c.exact ? 2 : 3) : c.exact ? 1 : 0;
-    if (mode == 3 && sizeof(T) == 4) return tbbox_run_dispatch(c, in, out, k);
+    // (k = 1: the one-level plane-sum kernel below streams faster than tbbox's k = 1)
+    if (mode == 3 && sizeof(T) == 4 && k >= 2) return tbbox_run_dispatch(c, in, out, k);
     if (mode == 3 && k >= 2) {  // SEP: the k-level skewed pipeline
         if (k == 3) return launchk<T, 3>(c, in, out);
         if (k == 4) return launchk<T, 4>(c, in, out);
