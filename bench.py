@@ -35,7 +35,10 @@ max_rel_deviation from EXACT (<= 1e-5 fp32, <= 1e-12 fp64).
 
 `value` is device-resident throughput (GStencil/s = points * K / time, the
 reference's Eq. 6, proj/src/metrics.cpp:8-20), timed with CUDA events on the
-streams the sweeps launch on (max over devices).  `e2e` is the same metric
+streams the sweeps launch on (max over devices).  At N=1 the K timed steps
+are captured once into a CUDA graph and replayed between the two events, so
+the device is not left waiting on the Python launch path between fused
+passes (--no-graph times the launches directly).  `e2e` is the same metric
 through the reference-facing call on host buffers in pinned memory (naive_run
 -> tsr_run at N=1, tsr_run_multi at N>1): H2D of the read buffer + K steps +
 D2H of both buffers.  `--impl reference` times the reference's own CPU path
@@ -357,10 +360,23 @@ def mode_check(ts, torch, cfg, k, host, state, per_gpu, dev, stream, kfused, mod
     for n in fused_groups(args.warmup, kfused):
         st2.advance(k, n, fused_steps=kfused, mode=other)
     torch.cuda.synchronize(dev)
+    groups = fused_groups(args.steps, kfused)
+    graph = None
+    if not args.no_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+                for n in groups:
+                    st2.advance(k, n, fused_steps=kfused, mode=other)
+        except Exception:
+            return None  # (the timed run fell back too)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for n in fused_groups(args.steps, kfused):
-        st2.advance(k, n, fused_steps=kfused, mode=other)
+    if graph is not None:
+        graph.replay()
+    else:
+        for n in groups:
+            st2.advance(k, n, fused_steps=kfused, mode=other)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms2 = e0.elapsed_time(e1)
@@ -450,24 +466,54 @@ def run_single(args, cfg):
         state.advance(k, n, fused_steps=kfused, mode=mode)
     torch.cuda.synchronize(dev)
 
+    # The K timed steps are captured once into a CUDA graph and replayed
+    # between two events: the device runs the launches back to back instead
+    # of waiting on Python/ctypes per launch (tens of microseconds, the size
+    # of a C1 launch).  The per-launch events of the direct path remain the
+    # fallback (--no-graph, or a capture the driver refuses).
+    graph, launches = None, 0
+    if not args.no_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+                for n in groups:
+                    launches += state.advance(k, n, fused_steps=kfused, mode=mode).kernel_launches
+        except Exception as e:  # the state advanced on paper only: rebuild it
+            print(f"graph capture unavailable ({e}); timing direct launches", file=sys.stderr)
+            graph, launches = None, 0
+            state = ts.DeviceGrid(host, dev)
+            state.advance(k, 1, fused_steps=kfused, mode=mode)
+            for n in fused_groups(args.warmup, kfused):
+                state.advance(k, n, fused_steps=kfused, mode=mode)
     sampler = ClockSampler([0])
     sampler.start()
     torch.cuda.synchronize(dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(groups) + 1)]
-    launches = 0
-    ev[0].record(stream)
-    for i, n in enumerate(groups):
-        st = state.advance(k, n, fused_steps=kfused, mode=mode)
-        launches += st.kernel_launches
-        ev[i + 1].record(stream)
-    torch.cuda.synchronize(dev)
-    clocks = sampler.stop()
-    elapsed_ms = ev[0].elapsed_time(ev[-1])
-    full = [ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(groups) if n == kfused]
-    launch_ms = statistics.mean(full) if full else elapsed_ms / max(1, len(groups))
+    if graph is not None:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        graph.replay()
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
+        clocks = sampler.stop()
+        elapsed_ms = ev[0].elapsed_time(ev[1])
+        launch_ms = elapsed_ms * kfused / args.steps
+        basis = "device time per k steps (CUDA-graph replay of the K steps)"
+    else:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(groups) + 1)]
+        ev[0].record(stream)
+        for i, n in enumerate(groups):
+            st = state.advance(k, n, fused_steps=kfused, mode=mode)
+            launches += st.kernel_launches
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        clocks = sampler.stop()
+        elapsed_ms = ev[0].elapsed_time(ev[-1])
+        full = [ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(groups) if n == kfused]
+        launch_ms = statistics.mean(full) if full else elapsed_ms / max(1, len(groups))
+        basis = "mean CUDA-event launch time"
     value = points * args.steps / (elapsed_ms / 1e3) / 1e9
-    roof, arith = roofline(cfg, args.config, k, points, kfused, launch_ms,
-                           "mean CUDA-event launch time")
+    roof, arith = roofline(cfg, args.config, k, points, kfused, launch_ms, basis)
 
     modes = None
     if not args.no_mode_check:
@@ -491,7 +537,8 @@ def run_single(args, cfg):
     cpu = None if args.no_cpu else cpu_baseline(cfg, 1)
     line = base_line(args, cfg, 1, mode, value, elapsed_ms)
     line.update({"plan": {"fused_steps": kfused,
-                          "engine": {1: "generic", 2: "tuned"}.get(engine, str(engine))},
+                          "engine": {1: "generic", 2: "tuned"}.get(engine, str(engine)),
+                          "launch": "cuda-graph replay" if graph is not None else "direct"},
                  "roofline": roof, "arith": arith, "modes": modes, "cpu_baseline": cpu,
                  "e2e": e2e, "gpu_launches": launches, "clocks": clocks})
     return line
@@ -679,6 +726,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="N>1: skip the one-GPU check")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N=1: time direct launches instead of a CUDA-graph replay of the K steps")
     ap.add_argument("--no-mode-check", action="store_true",
                     help="skip timing the other arithmetic mode and its deviation check")
     ap.add_argument("--share-devices", action="store_true",
