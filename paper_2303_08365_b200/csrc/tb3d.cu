@@ -617,8 +617,14 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.mshift = c.mirror_shift;
     for (int q = 0; q < 7; ++q) a.w[q] = static_cast<T>(c.taps->w[q]);
     if (c.mirror) {
-        TSR_CUDA_TRY(cudaFuncSetAttribute(tb3d_kernel<T, K, EXACT, G, EARLY0, true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        static bool attr_set[64] = {};  // per device, once
+        int dev = 0;
+        TSR_CUDA_TRY(cudaGetDevice(&dev));
+        if (dev >= 64 || !attr_set[dev]) {
+            TSR_CUDA_TRY(cudaFuncSetAttribute(tb3d_kernel<T, K, EXACT, G, EARLY0, true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            if (dev < 64) attr_set[dev] = true;
+        }
         tb3d_kernel<T, K, EXACT, G, EARLY0, true><<<grid, G::NT, bytes, c.stream>>>(
             static_cast<T*>(out), map, a);
     } else {

@@ -513,8 +513,14 @@ Status launch_k(const LaunchCtx& c, const void* in, void* out) {
     a.mshift = c.mirror_shift;
     a.w = static_cast<T>(c.taps->w[0]);
     if (c.mirror) {
-        TSR_CUDA_TRY(cudaFuncSetAttribute(tbbox_kernel<K, G, true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        static bool attr_set[64] = {};  // per device, once
+        int dev = 0;
+        TSR_CUDA_TRY(cudaGetDevice(&dev));
+        if (dev >= 64 || !attr_set[dev]) {
+            TSR_CUDA_TRY(cudaFuncSetAttribute(tbbox_kernel<K, G, true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            if (dev < 64) attr_set[dev] = true;
+        }
         tbbox_kernel<K, G, true><<<grid, G::NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);
     } else {
         tbbox_kernel<K, G, false><<<grid, G::NT, bytes, c.stream>>>(static_cast<T*>(out), map, a);

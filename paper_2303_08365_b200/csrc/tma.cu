@@ -1,4 +1,7 @@
 // tma.cu — host helpers behind tma.cuh.
+#include <mutex>
+#include <vector>
+
 #include "tma.cuh"
 
 namespace tsr {
@@ -35,6 +38,31 @@ int pick_chunk(int64_t n0, int64_t tiles, int64_t slots, int overlap, int min_ch
         }
     }
     return (int)best_chunk;
+}
+
+namespace {
+struct OccEntry {
+    const void* fn;
+    int dev, threads, smem, per_sm, nsm;
+};
+std::mutex g_occ_mu;
+std::vector<OccEntry> g_occ;
+}  // namespace
+
+bool occupancy_cached(const void* fn, int dev, int threads, int smem, int* per_sm, int* nsm) {
+    std::lock_guard<std::mutex> lock(g_occ_mu);
+    for (const OccEntry& e : g_occ)
+        if (e.fn == fn && e.dev == dev && e.threads == threads && e.smem == smem) {
+            *per_sm = e.per_sm;
+            *nsm = e.nsm;
+            return true;
+        }
+    return false;
+}
+
+void occupancy_store(const void* fn, int dev, int threads, int smem, int per_sm, int nsm) {
+    std::lock_guard<std::mutex> lock(g_occ_mu);
+    g_occ.push_back(OccEntry{fn, dev, threads, smem, per_sm, nsm});
 }
 
 }  // namespace tsr

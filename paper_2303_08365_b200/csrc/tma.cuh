@@ -77,14 +77,24 @@ Status make_tmap_3d(const Geo& g, const void* base, int box_w, int box_h, CUtens
 
 // Resident CTAs per SM for `kernel` (after raising its dynamic smem limit)
 // and the SM count of the current device.
+// Cached per kernel (function address) and device: the first call sets the
+// shared-memory limit and queries the driver; the slab runtime launches
+// several sweeps per round from one host thread, so per-launch driver
+// queries would be host time on every round.
+bool occupancy_cached(const void* fn, int dev, int threads, int smem, int* per_sm, int* nsm);
+void occupancy_store(const void* fn, int dev, int threads, int smem, int per_sm, int nsm);
+
 template <typename K>
 Status occupancy(K kernel, int threads, int smem, int* per_sm, int* nsm) {
     int dev = 0;
     TSR_CUDA_TRY(cudaGetDevice(&dev));
+    const void* fn = reinterpret_cast<const void*>(kernel);
+    if (occupancy_cached(fn, dev, threads, smem, per_sm, nsm)) return Status::Ok();
     TSR_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     TSR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kernel, threads, smem));
     TSR_CUDA_TRY(cudaDeviceGetAttribute(nsm, cudaDevAttrMultiProcessorCount, dev));
     if (*per_sm < 1) return Status::Err(TSR_ECUDA, "kernel cannot be resident on an SM");
+    occupancy_store(fn, dev, threads, smem, *per_sm, *nsm);
     return Status::Ok();
 }
 
