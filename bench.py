@@ -444,6 +444,35 @@ def base_line(args, cfg, n, mode, value, elapsed_ms):
             "data": DATA, "config": bench_config(cfg, n, mode)}
 
 
+def pcie_bound(torch, dev, h2d_bytes, d2h_bytes, device_s, wall_s, updates):
+    """The e2e ceiling of one tsr_run call: its host<->device bytes at the
+    pinned-copy rates measured here (256 MiB copies, best of 3, CUDA events)
+    plus the device-resident time of the same steps.  `frac` = that bound over
+    the measured wall time (1.0 = the call runs at the PCIe + kernel floor)."""
+    n = 256 << 20
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    devb = torch.empty(n, dtype=torch.uint8, device=dev)
+    rates = {}
+    for name, dst, src in (("h2d", devb, host), ("d2h", host, devb)):
+        best = None
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        rates[name] = n / (best / 1e3) / 1e9
+    del host, devb
+    floor_s = h2d_bytes / (rates["h2d"] * 1e9) + d2h_bytes / (rates["d2h"] * 1e9) + device_s
+    return {"h2d_gbs": round(rates["h2d"], 2), "d2h_gbs": round(rates["d2h"], 2),
+            "floor_s": round(floor_s, 4), "bound_value": round(updates / floor_s / 1e9, 3),
+            "frac": round(floor_s / wall_s, 4),
+            "basis": "per-call bytes at the measured pinned-copy rates + device time of the "
+                     "same steps (timed region above)"}
+
+
 def run_single(args, cfg):
     """N = 1: DeviceGrid (tsr_advance) on cuda:0, CUDA events per fused pass."""
     import torch
@@ -532,7 +561,9 @@ def run_single(args, cfg):
                "h2d_bytes_per_step": round(st.h2d_bytes / args.steps, 1),
                "d2h_bytes_per_step": round(st.d2h_bytes / args.steps, 1),
                "call": "paper_2303_08365_b200.run_gpu(pinned Grid) -> tsr_run",
-               "wall_s": round(wall, 4)}
+               "wall_s": round(wall, 4),
+               "pcie": pcie_bound(torch, dev, st.h2d_bytes, st.d2h_bytes,
+                                  elapsed_ms / 1e3, wall, points * args.steps)}
         del hg
     cpu = None if args.no_cpu else cpu_baseline(cfg, 1)
     line = base_line(args, cfg, 1, mode, value, elapsed_ms)

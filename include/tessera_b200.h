@@ -140,9 +140,12 @@ int tsr_layout_of(const tsr_grid* g, tsr_layout* out);
  * host buffers of a BasicGrid<T>, `parity` its read buffer.  On return the
  * buffers are exactly as naive_run leaves them: buffer(parity ^ (steps&1))
  * holds step T, the other buffer holds step T-1, halo cells untouched.  The
- * caller flips its parity `steps` times.  Requires the halo cells of both
- * buffers to be equal (every reference constructor guarantees it).  Pinned
- * host buffers make the copies run at full PCIe rate. */
+ * caller flips its parity `steps` times.  When the halo cells of the two
+ * buffers are equal (every reference constructor guarantees it) one buffer
+ * is uploaded and the steps are fused; when they differ, both buffers are
+ * uploaded and every step is its own sweep reading its read buffer's halo,
+ * as naive_run does (stats->fused_steps = 1).  Pinned host buffers make the
+ * copies run at full PCIe rate. */
 int tsr_run(const tsr_kernel* k, const tsr_grid* g, void* buf0, void* buf1, int32_t parity,
             int64_t steps, const tsr_opts* opts, tsr_stats* stats);
 

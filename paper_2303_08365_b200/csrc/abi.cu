@@ -6,11 +6,13 @@
 #include <array>
 #include <functional>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <random>
 #include <sstream>
+#include <thread>
 #include <vector>
 
 #include "runtime.cuh"
@@ -218,13 +220,12 @@ Status download(const Geo& g, const void* dev, void* host, bool interior_only, c
 }
 
 // True when the halo shells of the two host buffers are bitwise equal.
-bool halos_equal(const Geo& g, const void* b0, const void* b1) {
+static bool halos_equal_rows(const Geo& g, const void* b0, const void* b1, int64_t r_lo, int64_t r_hi) {
     const char* a = static_cast<const char*>(b0);
     const char* b = static_cast<const char*>(b1);
     const int64_t rows1 = g.n[1] + 2 * g.h[1];
-    const int64_t rows = (g.n[0] + 2 * g.h[0]) * rows1;
     const int64_t rowlen = g.hpitch[1] * g.esize;
-    for (int64_t r = 0; r < rows; ++r) {
+    for (int64_t r = r_lo; r < r_hi; ++r) {
         const int64_t r0 = r / rows1, r1 = r % rows1;
         const int64_t off = (r0 * g.hpitch[0] + r1 * g.hpitch[1]) * g.esize;
         const bool halo_row = r0 < g.h[0] || r0 >= g.n[0] + g.h[0] || r1 < g.h[1] ||
@@ -238,6 +239,26 @@ bool halos_equal(const Geo& g, const void* b0, const void* b1) {
             if (std::memcmp(a + tail, b + tail, hb) != 0) return false;
         }
     }
+    return true;
+}
+
+// The comparison touches a few bytes of every row of both buffers (page- and
+// TLB-bound: ~8 ms for two 1 GB buffers on one thread); rows are split over
+// up to 8 host threads, so it ends before the first upload pieces do.
+bool halos_equal(const Geo& g, const void* b0, const void* b1) {
+    const int64_t rows = (g.n[0] + 2 * g.h[0]) * (g.n[1] + 2 * g.h[1]);
+    const int nt = static_cast<int>(std::min<int64_t>(
+        std::max(1u, std::min(8u, std::thread::hardware_concurrency())), rows / 4096 + 1));
+    if (nt == 1) return halos_equal_rows(g, b0, b1, 0, rows);
+    std::vector<std::thread> th;
+    std::vector<char> ok(nt, 1);
+    for (int i = 0; i < nt; ++i)
+        th.emplace_back([&, i] {
+            ok[i] = halos_equal_rows(g, b0, b1, rows * i / nt, rows * (i + 1) / nt);
+        });
+    for (auto& x : th) x.join();
+    for (char v : ok)
+        if (!v) return false;
     return true;
 }
 
@@ -321,6 +342,12 @@ struct DeviceCache {
     // allocated; without it the downloads are pitched 3-D copies)
     void* stage = nullptr;
     int64_t stage_bytes = 0;
+    // chunked round trip (run_chunked): compute and device->host streams,
+    // an event pool and the two window sets
+    cudaStream_t s_comp = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> pool;
+    void* pipe = nullptr;
+    int64_t pipe_bytes = 0;
 };
 std::mutex g_cache_mu;
 std::vector<DeviceCache> g_cache;
@@ -391,6 +418,193 @@ tsr_opts opts_or_default(const tsr_opts* o) {
 
 namespace {
 
+// ---- chunked host round trip ------------------------------------------
+// A short run's tsr_run is PCIe-bound: one buffer up, two down.  Step T at a
+// plane of the outermost axis depends only on the planes within T*r of it, so
+// for T*r small against that axis the grid is cut into chunks of planes, each
+// advanced T steps on its own window (the chunk widened by T*r planes per side:
+// the window's edge planes act as a frozen halo whose error moves inward r
+// planes per step and never reaches the chunk).  Window j computes once the
+// planes it reads are uploaded, and its chunk of steps T and T-1 goes down
+// while later windows compute and later pieces go up: host->device and
+// device->host copies run concurrently (PCIe is full duplex) instead of one
+// after the other.  Each point runs the same per-point arithmetic as the
+// whole-grid run (same engine, same fused depth), so the result is identical.
+struct Chunks {
+    int ax = 0;           // normalised outermost axis (3 - dims)
+    int64_t n0 = 0, h0 = 0, margin = 0, size = 0;
+    int nchunks = 0;
+    int64_t piece = 0;    // host planes per upload piece
+    int npieces = 0;
+    int64_t hplane = 0;   // host elements per plane
+    int64_t win_elems = 0, out_elems = 0;  // per buffer of one window set
+};
+
+bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
+    if (g.dims < 2) return false;
+    // TSR_RUN_CHUNKED: 0 = never, 1 = whenever there are >= 3 chunks, unset =
+    // grids of >= 256 MiB per buffer (below that the transfers are a few ms
+    // and the extra launches cancel the overlap: 4096^2 fp64 8.4 ms either way)
+    const char* env = std::getenv("TSR_RUN_CHUNKED");
+    if (env && *env == '0') return false;
+    if (!(env && *env == '1') && g.host_elements * g.esize < (int64_t(256) << 20)) return false;
+    Chunks c;
+    c.ax = 3 - g.dims;
+    c.n0 = g.n[c.ax];
+    c.h0 = g.h[c.ax];
+    c.margin = steps * std::max(1, t.radius);
+    // chunks of 2*T*r planes (windows twice the chunk): the first download
+    // starts after a small share of the upload; at most 32 chunks
+    c.size = std::max<int64_t>({16, 2 * c.margin, (c.n0 + 31) / 32});
+    c.nchunks = static_cast<int>(c.n0 / c.size);  // the last chunk takes the remainder
+    if (c.nchunks < 3) return false;
+    c.hplane = g.hpitch[c.ax];
+    c.piece = c.size;
+    c.npieces = static_cast<int>((c.n0 + 2 * c.h0 + c.piece - 1) / c.piece);
+    *ch = c;
+    return true;
+}
+
+tsr_grid window_grid(const tsr_grid& gg, int64_t planes) {
+    tsr_grid w = gg;
+    w.extent[0] = planes;
+    return w;
+}
+
+Status chunk_resources(const Geo& g, Chunks& ch, DeviceCache* c) {
+    if (!c->s_comp) {
+        TSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+        TSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+    }
+    const size_t need = static_cast<size_t>(ch.npieces + 4 * ch.nchunks);
+    while (c->pool.size() < need) {
+        cudaEvent_t e;
+        TSR_CUDA_TRY(cudaEventCreate(&e));
+        c->pool.push_back(e);
+    }
+    // window device buffers: the widest window's pitched layout (same row
+    // pitch as the whole grid: only the plane count differs)
+    const int64_t last = ch.n0 - (ch.nchunks - 1) * ch.size;  // the widest chunk
+    const int64_t wplanes = std::min(ch.n0, last + 2 * ch.margin);
+    ch.win_elems = (wplanes + 2 * ch.h0) * g.pitch[ch.ax];
+    ch.out_elems = last * ch.hplane;
+    const int64_t bytes = 2 * (2 * ch.win_elems + 2 * ch.out_elems) * g.esize;
+    if (c->pipe_bytes < bytes) {
+        if (c->pipe) cudaFree(c->pipe);
+        c->pipe = nullptr;
+        c->pipe_bytes = 0;
+        if (cudaMalloc(&c->pipe, bytes) != cudaSuccess) {
+            cudaGetLastError();  // no room: the unchunked round trip
+            return Status::Ok();
+        }
+        c->pipe_bytes = bytes;
+    }
+    return Status::Ok();
+}
+
+Status run_chunked(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_opts& o,
+                   DeviceCache* c, void* const host[2], int parity, int64_t steps,
+                   const Chunks& ch, tsr_stats* st) {
+    // the whole grid's plan (engine, fused depth) for every window
+    Plan p;
+    Status r = plan_for(g, t, o, p);
+    if (!r.ok()) return r;
+    tsr_opts wo = o;
+    wo.fused_steps = p.k;
+    const int64_t es = g.esize;
+    cudaEvent_t* ev_in = c->pool.data();
+    cudaEvent_t* ev_c0 = ev_in + ch.npieces;
+    cudaEvent_t* ev_c1 = ev_c0 + ch.nchunks;
+    cudaEvent_t* ev_rel = ev_c1 + ch.nchunks;
+    cudaEvent_t* ev_out = ev_rel + ch.nchunks;
+    const int pfinal = parity ^ static_cast<int>(steps & 1);
+    tsr_stats local{};
+    int64_t d2h = 0;
+    for (int j = 0; j < ch.nchunks; ++j) {
+        char* set = static_cast<char*>(c->pipe) + (j & 1) * (2 * ch.win_elems + 2 * ch.out_elems) * es;
+        void* wbuf[2] = {set, set + ch.win_elems * es};
+        char* ostage[2] = {set + 2 * ch.win_elems * es, set + (2 * ch.win_elems + ch.out_elems) * es};
+        const int64_t a = j * ch.size, b = j + 1 == ch.nchunks ? ch.n0 : a + ch.size;
+        const int64_t wa = std::max<int64_t>(0, a - ch.margin);
+        const int64_t wb = std::min(ch.n0, b + ch.margin);
+        Geo gw;
+        r = make_geo(window_grid(gg, wb - wa), gw);
+        if (!r.ok()) return r;
+        // host planes [wa, wb + 2 h0) of the read buffer must have arrived
+        const int last_piece = static_cast<int>((wb + 2 * ch.h0 - 1) / ch.piece);
+        TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_comp, ev_in[last_piece], 0));
+        if (j >= 2) TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_comp, ev_out[j - 2], 0));
+        TSR_CUDA_TRY(cudaEventRecord(ev_c0[j], c->s_comp));
+        r = relayout(gw, static_cast<const char*>(c->d[1]) + wa * ch.hplane * es, wbuf[0], true,
+                     c->s_comp);
+        if (!r.ok()) return r;
+        r = halo_copy(gw, wbuf[0], wbuf[1], c->s_comp);
+        if (!r.ok()) return r;
+        int cur = 0;
+        tsr_stats ws{};
+        r = advance(gw, t, wo, wbuf[0], wbuf[1], &cur, steps, true, c->s_comp, &ws);
+        if (!r.ok()) return r;
+        TSR_CUDA_TRY(cudaEventRecord(ev_c1[j], c->s_comp));
+        if (j == 0) {
+            local.rounds = ws.rounds;
+            local.trailing_steps = ws.trailing_steps;
+            local.fused_steps = ws.fused_steps;
+            local.engine = ws.engine;
+        }
+        local.kernel_launches += ws.kernel_launches;
+        // planes [a, b) of steps T and T-1 into host layout
+        Geo go = gw;
+        go.n[ch.ax] = b - a;
+        go.h[ch.ax] = 0;
+        const int64_t src_off = (a - wa + ch.h0) * gw.pitch[ch.ax] * es;
+        const int nout = steps >= 2 ? 2 : 1;
+        for (int q = 0; q < nout; ++q) {
+            r = relayout(go, static_cast<const char*>(wbuf[q == 0 ? cur : 1 - cur]) + src_off,
+                         ostage[q], false, c->s_comp);
+            if (!r.ok()) return r;
+        }
+        TSR_CUDA_TRY(cudaEventRecord(ev_rel[j], c->s_comp));
+        TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_out, ev_rel[j], 0));
+        const int64_t n = (b - a) * ch.hplane * es, dst = (a + ch.h0) * ch.hplane * es;
+        for (int q = 0; q < nout; ++q) {
+            TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(host[q == 0 ? pfinal : 1 - pfinal]) + dst,
+                                         ostage[q], n, cudaMemcpyDeviceToHost, c->s_out));
+            d2h += n;
+        }
+        TSR_CUDA_TRY(cudaEventRecord(ev_out[j], c->s_out));
+    }
+    TSR_CUDA_TRY(cudaStreamSynchronize(c->s_out));
+    TSR_CUDA_TRY(cudaStreamSynchronize(c->s_comp));
+    TSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    double ms = 0;
+    for (int j = 0; j < ch.nchunks; ++j) {
+        float m = 0.f;
+        TSR_CUDA_TRY(cudaEventElapsedTime(&m, ev_c0[j], ev_c1[j]));
+        ms += m;
+    }
+    if (const char* tr = std::getenv("TSR_CHUNK_TRACE"); tr && *tr == '1') {
+        // per-window timeline (ms from the first upload piece's completion)
+        for (int j = 0; j < ch.nchunks; ++j) {
+            float t[4] = {0, 0, 0, 0};
+            cudaEventElapsedTime(&t[0], ev_in[0], ev_c0[j]);
+            cudaEventElapsedTime(&t[1], ev_in[0], ev_c1[j]);
+            cudaEventElapsedTime(&t[2], ev_in[0], ev_rel[j]);
+            cudaEventElapsedTime(&t[3], ev_in[0], ev_out[j]);
+            std::fprintf(stderr, "chunk %d: start %.2f swept %.2f relaid %.2f downloaded %.2f\n", j,
+                         t[0], t[1], t[2], t[3]);
+        }
+        float tl = 0;
+        cudaEventElapsedTime(&tl, ev_in[0], ev_in[ch.npieces - 1]);
+        std::fprintf(stderr, "pieces %d, last piece uploaded %.2f\n", ch.npieces, tl);
+    }
+    local.point_updates = g.interior() * steps;
+    local.device_ms = ms;
+    local.h2d_bytes = g.host_elements * es;
+    local.d2h_bytes = d2h;
+    if (st) *st = local;
+    return Status::Ok();
+}
+
 Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, int parity,
                 int64_t steps, const tsr_opts* oo, tsr_stats* st) {
     if (!kk || !gg || !b0 || !b1) return Status::Err(TSR_EINVAL, "null argument");
@@ -407,15 +621,9 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     const tsr_opts o = opts_or_default(oo);
     if (st) *st = tsr_stats{};
     if (steps == 0) return Status::Ok();
-    const char* halo_msg =
-        "halo cells differ between the two buffers (Dirichlet halo must be set in both, as "
-        "set_both/fill do)";
     DeviceGuard guard;
     r = guard.enter(o.device);
-    if (!r.ok()) {  // argument errors take precedence over device errors
-        if (!halos_equal(g, b0, b1)) return Status::Err(TSR_EINVAL, halo_msg);
-        return r;
-    }
+    if (!r.ok()) return r;
     int dev = 0;
     TSR_CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(g_cache_mu);
@@ -428,26 +636,58 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     // is 1.4x faster than pitched 3-D copies of 4 KB rows.
     const int64_t hbytes = g.host_elements * g.esize;
     const bool staged_up = c->bytes >= hbytes;  // d[1] can hold the host layout
-    if (staged_up) {
+    Chunks ch;
+    bool chunked = staged_up && plan_chunks(g, t, steps, &ch);
+    if (chunked) {
+        r = chunk_resources(g, ch, c);
+        if (!r.ok()) return r;
+        chunked = c->pipe != nullptr;
+    }
+    if (chunked) {
+        // the read buffer goes up in pieces, an event after each, so window
+        // j computes as soon as the planes it reads have arrived
+        const int64_t pb = ch.piece * ch.hplane * g.esize;
+        for (int i = 0; i < ch.npieces; ++i) {
+            const int64_t off = i * pb, n = std::min(pb, hbytes - off);
+            TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d[1]) + off,
+                                         static_cast<const char*>(host[parity]) + off, n,
+                                         cudaMemcpyHostToDevice, c->stream));
+            TSR_CUDA_TRY(cudaEventRecord(c->pool[i], c->stream));
+        }
+    } else if (staged_up) {
         TSR_CUDA_TRY(cudaMemcpyAsync(c->d[1], host[parity], hbytes, cudaMemcpyHostToDevice,
                                      c->stream));
-        r = relayout(g, c->d[1], c->d[0], true, c->stream);
     } else {
         r = upload(g, host[parity], c->d[0], c->stream);
+        if (!r.ok()) return r;
     }
-    if (!r.ok()) return r;
-    // The host-side precondition check (it touches every page of both
-    // buffers: ~10-20 ms at 512^3) runs while the upload is in flight.
-    if (!halos_equal(g, b0, b1)) {
-        cudaStreamSynchronize(c->stream);
-        return Status::Err(TSR_EINVAL, halo_msg);
+    // The host-side halo comparison (it touches every page of both buffers:
+    // ~10-20 ms at 512^3) runs while the upload is in flight.
+    const bool same_halo = halos_equal(g, b0, b1);
+    if (chunked && same_halo) return run_chunked(*gg, g, t, o, c, host, parity, steps, ch, st);
+    if (staged_up) {
+        r = relayout(g, c->d[1], c->d[0], true, c->stream);
+        if (!r.ok()) return r;
     }
-    r = halo_copy(g, c->d[0], c->d[1], c->stream);
+    int64_t h2d = hbytes;
+    tsr_opts run_o = o;
+    if (same_halo) {
+        // one upload + a device-side halo copy is exact
+        r = halo_copy(g, c->d[0], c->d[1], c->stream);
+    } else {
+        // naive_run (naive.hpp:96-100) reads every step's halo from that
+        // step's read buffer: with two different halos the write buffer is
+        // uploaded too (its halo is what the odd steps read) and every step
+        // is its own sweep, which reads the halo of its input buffer.
+        r = upload(g, host[1 - parity], c->d[1], c->stream);
+        h2d += hbytes;
+        run_o.fused_steps = 1;
+    }
     if (!r.ok()) return r;
     int cur = 0;
     tsr_stats local{};
     TSR_CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
-    r = advance(g, t, o, c->d[0], c->d[1], &cur, steps, true, c->stream, &local);
+    r = advance(g, t, run_o, c->d[0], c->d[1], &cur, steps, true, c->stream, &local);
     if (!r.ok()) return r;
     TSR_CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
     const int pfinal = parity ^ static_cast<int>(steps & 1);
@@ -460,9 +700,10 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
         else
             cudaGetLastError();  // no room: pitched copies below
     }
-    // The staged path copies the whole host layout back: its halo cells are
-    // the uploaded ones, equal in both host buffers (checked above), so the
-    // host halo is rewritten with its own bytes.
+    // The staged path copies the whole host layout back: each device
+    // buffer's halo cells are its own host buffer's (uploaded, or copied
+    // from the other buffer when the two halos are equal), so the host halo
+    // is rewritten with its own bytes.
     auto fetch = [&](int which, int into, int64_t* bytes) -> Status {
         if (c->stage) {
             Status q = relayout(g, c->d[which], c->stage, false, c->stream);
@@ -486,7 +727,7 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     float ms = 0.f;
     TSR_CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
     local.device_ms = ms;
-    local.h2d_bytes = g.host_elements * g.esize;
+    local.h2d_bytes = h2d;
     local.d2h_bytes = d2h;
     if (st) *st = local;
     return Status::Ok();
@@ -588,6 +829,13 @@ int tsr_release_cache(void) {
         for (cudaEvent_t& e : c.ev)
             if (e) cudaEventDestroy(e), e = nullptr;
         if (c.stream) cudaStreamDestroy(c.stream), c.stream = nullptr;
+        if (c.pipe) cudaFree(c.pipe);
+        c.pipe = nullptr;
+        c.pipe_bytes = 0;
+        for (cudaEvent_t e : c.pool) cudaEventDestroy(e);
+        c.pool.clear();
+        if (c.s_comp) cudaStreamDestroy(c.s_comp), c.s_comp = nullptr;
+        if (c.s_out) cudaStreamDestroy(c.s_out), c.s_out = nullptr;
     }
     cudaSetDevice(prev);
     return TSR_OK;

@@ -102,6 +102,3 @@ def test_run_validates_before_touching_the_device(ts):
         ts.naive_run(g, ts.heat_coefficients(0.2), -1)
     ts.naive_run(g, ts.heat_coefficients(0.2), 0)  # T = 0 is a no-op
     assert g.parity == 0
-    g.buffer(1)[0] = 1.0  # halo differs between the buffers
-    with pytest.raises(ValueError, match="halo"):
-        ts.naive_run(g, ts.heat_coefficients(0.2), 1)
