@@ -4,6 +4,7 @@
 // driver and engine dispatch.
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <functional>
 #include <cmath>
 #include <cstdio>
@@ -573,9 +574,12 @@ Status run_chunked(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_
         }
         TSR_CUDA_TRY(cudaEventRecord(ev_out[j], c->s_out));
     }
+    const auto t_enq = std::chrono::steady_clock::now();
     TSR_CUDA_TRY(cudaStreamSynchronize(c->s_out));
     TSR_CUDA_TRY(cudaStreamSynchronize(c->s_comp));
     TSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const double wait_ms = std::chrono::duration<double, std::milli>(
+                               std::chrono::steady_clock::now() - t_enq).count();
     double ms = 0;
     for (int j = 0; j < ch.nchunks; ++j) {
         float m = 0.f;
@@ -595,7 +599,8 @@ Status run_chunked(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_
         }
         float tl = 0;
         cudaEventElapsedTime(&tl, ev_in[0], ev_in[ch.npieces - 1]);
-        std::fprintf(stderr, "pieces %d, last piece uploaded %.2f\n", ch.npieces, tl);
+        std::fprintf(stderr, "pieces %d, last piece uploaded %.2f; host waited %.2f ms\n",
+                     ch.npieces, tl, wait_ms);
     }
     local.point_updates = g.interior() * steps;
     local.device_ms = ms;
@@ -663,7 +668,12 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     }
     // The host-side halo comparison (it touches every page of both buffers:
     // ~10-20 ms at 512^3) runs while the upload is in flight.
+    const auto t_enq = std::chrono::steady_clock::now();
     const bool same_halo = halos_equal(g, b0, b1);
+    if (const char* tr = std::getenv("TSR_CHUNK_TRACE"); tr && *tr == '1')
+        std::fprintf(stderr, "run_host: chunked=%d halo check %.2f ms\n", int(chunked),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                               t_enq).count());
     if (chunked && same_halo) return run_chunked(*gg, g, t, o, c, host, parity, steps, ch, st);
     if (staged_up) {
         r = relayout(g, c->d[1], c->d[0], true, c->stream);
@@ -734,6 +744,11 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
 }
 
 }  // namespace
+
+Status run_host_single(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b1, int parity,
+                       int64_t steps, const tsr_opts* o, tsr_stats* st) {
+    return run_host(k, g, b0, b1, parity, steps, o, st);
+}
 
 template <typename T>
 void fill_random_t(const Geo& g, T* b0, T* b1, uint64_t seed, double lo, double hi,

@@ -743,11 +743,15 @@ Status run_multi(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, i
     if (st) *st = tsr_stats{};
     void* host[2] = {b0, b1};
     const bool equal_halos = halos_equal(g, b0, b1);
-    if (keep_prev && !equal_halos)
-        return Status::Err(TSR_EINVAL,
-                           "halo cells differ between the two buffers (Dirichlet halo must be "
-                           "set in both, as set_both/fill do)");
     if (steps == 0) return Status::Ok();
+    if (keep_prev && !equal_halos) {
+        // naive_run semantics with two different halos (every step reads its
+        // read buffer's halo): one device, one sweep per step (run_host)
+        tsr_opts o1 = o;
+        o1.ngpus = 1;
+        o1.device = part && part->devices ? part->devices[0] : -1;
+        return run_host_single(kk, gg, b0, b1, parity, steps, &o1, st);
+    }
     DeviceGuard guard;
     r = guard.enter(-1);
     if (!r.ok()) return r;

@@ -34,6 +34,10 @@ Status download(const Geo& g, const void* dev, void* host, bool interior_only, c
 // True when the halo shells of the two host buffers are bitwise equal.
 bool halos_equal(const Geo& g, const void* b0, const void* b1);
 
+// tsr_run on one device (the naive_run drop-in over host buffers).
+Status run_host_single(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b1, int parity,
+                       int64_t steps, const tsr_opts* o, tsr_stats* st);
+
 // Sets the calling thread's device for a scope (and checks one exists).
 struct DeviceGuard {
     int prev = -1;

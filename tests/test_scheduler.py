@@ -377,3 +377,20 @@ def test_slabs_fast_equal_one_device_fast(ts, orc, name, extent, dt, fused, P):
     assert g.parity == one.parity
     for w in (0, 1):
         assert g.interior_view(w).tobytes() == one.interior_view(w).tobytes(), w
+
+
+@pytest.mark.gpu
+def test_run_multi_differing_halos(ts, orc):
+    """Two buffers with different halo cells: tsr_run_multi honours naive_run's
+    per-step halo (each step reads its read buffer's halo) by running on one
+    device, one sweep per step; both buffers bitwise the oracle's."""
+    k = _kernel(ts, "Heat-3D")
+    g = random_grid(ts, orc, [48, 20, 40], [1, 1, 1], 503)
+    g.padded(0)[0] = 0.5
+    g.padded(1)[0] = -0.75
+    ref = g.copy()
+    st = ts.run_multi(g, k, 7, 2, devices=_devices(2))
+    orc.naive_run(ref, k, 7)
+    assert st.fused_steps == 1 and g.parity == ref.parity
+    for w in (0, 1):
+        assert g.buffer(w).tobytes() == ref.buffer(w).tobytes(), w
