@@ -456,7 +456,7 @@ bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     c.margin = steps * std::max(1, t.radius);
     // chunks of 2*T*r planes (windows twice the chunk): the first download
     // starts after a small share of the upload; at most 32 chunks
-    c.size = std::max<int64_t>({16, 2 * c.margin, (c.n0 + 31) / 32});
+    c.size = std::max<int64_t>({16, 2 * c.margin, (c.n0 + 31) / 32, 2 * c.h0 + 1});
     c.nchunks = static_cast<int>(c.n0 / c.size);  // the last chunk takes the remainder
     if (c.nchunks < 3) return false;
     c.hplane = g.hpitch[c.ax];
@@ -503,9 +503,26 @@ Status chunk_resources(const Geo& g, Chunks& ch, DeviceCache* c) {
     return Status::Ok();
 }
 
+Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_opts& o,
+                        DeviceCache* c, void* const host[2], int parity, int64_t steps,
+                        const Chunks& ch, tsr_stats* st);
+
 Status run_chunked(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_opts& o,
                    DeviceCache* c, void* const host[2], int parity, int64_t steps,
                    const Chunks& ch, tsr_stats* st) {
+    Status r = run_chunked_impl(gg, g, t, o, c, host, parity, steps, ch, st);
+    if (!r.ok()) {
+        // nothing queued may still write the caller's host buffers
+        cudaStreamSynchronize(c->s_out);
+        cudaStreamSynchronize(c->s_comp);
+        cudaStreamSynchronize(c->stream);
+    }
+    return r;
+}
+
+Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_opts& o,
+                        DeviceCache* c, void* const host[2], int parity, int64_t steps,
+                        const Chunks& ch, tsr_stats* st) {
     // the whole grid's plan (engine, fused depth) for every window
     Plan p;
     Status r = plan_for(g, t, o, p);

@@ -537,15 +537,16 @@ def test_box27_separable_fast_within_tolerance(ts, orc, dt, fused):
         assert halos_equal(a, b)
 
 
-@pytest.mark.parametrize("name,dt,extent,mode", [
-    ("Heat-3D", "f64", [200, 40, 70], "exact"),
-    ("Heat-3D", "f64", [131, 33, 65], "fast"),
-    ("Box-3D27P", "f32", [150, 37, 130], "fast"),
-    ("Box-3D27P", "f64", [97, 20, 33], "exact"),
-    ("Heat-2D", "f64", [300, 90], "exact"),
-    ("Box-2D9P", "f64", [257, 130], "fast"),
+@pytest.mark.parametrize("name,dt,extent,mode,halo", [
+    ("Heat-3D", "f64", [200, 40, 70], "exact", None),
+    ("Heat-3D", "f64", [131, 33, 65], "fast", None),
+    ("Heat-3D", "f64", [150, 21, 40], "exact", [9, 1, 2]),  # halo wider than a chunk's margin
+    ("Box-3D27P", "f32", [150, 37, 130], "fast", None),
+    ("Box-3D27P", "f64", [97, 20, 33], "exact", None),
+    ("Heat-2D", "f64", [300, 90], "exact", None),
+    ("Box-2D9P", "f64", [257, 130], "fast", None),
 ])
-def test_chunked_round_trip(ts, orc, monkeypatch, name, dt, extent, mode):
+def test_chunked_round_trip(ts, orc, monkeypatch, name, dt, extent, mode, halo):
     """tsr_run's chunked round trip (short runs: chunks of the outermost axis
     advanced on windows widened by T*r planes, uploads, windows and downloads
     overlapped) returns exactly what the whole-grid round trip returns, and
@@ -554,7 +555,7 @@ def test_chunked_round_trip(ts, orc, monkeypatch, name, dt, extent, mode):
     k = ts.find_benchmark(name).kernel
 
     def grid(steps, parity):
-        g = random_grid(ts, orc, extent, [k.radius] * k.dims, 7, dt)
+        g = random_grid(ts, orc, extent, halo or [k.radius] * k.dims, 7, dt)
         for w in (0, 1):
             g.padded(w)[0] = 0.5
         if parity:
