@@ -444,11 +444,20 @@ struct Chunks {
 bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     if (g.dims < 2) return false;
     // TSR_RUN_CHUNKED: 0 = never, 1 = whenever there are >= 3 chunks, unset =
-    // grids of >= 256 MiB per buffer (below that the transfers are a few ms
-    // and the extra launches cancel the overlap: 4096^2 fp64 8.4 ms either way)
+    // grids of >= 64 MiB per buffer (TSR_CHUNK_MIN_MB; below that the copies
+    // take a few ms and the extra launches cancel the overlap).  At most 16
+    // chunks below 1 GiB per buffer, 32 above (TSR_CHUNKS_MAX), from a sweep
+    // at T = 20 (tools/probe/chunk_sweep.py): 4096^2 fp64 7.8 -> 5.9 ms with
+    // 16 (7.1 with 32), 16384^2 121.6 -> 84.2 ms with 32 (85.8 with 16).
+    const int64_t bytes = g.host_elements * g.esize;
     const char* env = std::getenv("TSR_RUN_CHUNKED");
     if (env && *env == '0') return false;
-    if (!(env && *env == '1') && g.host_elements * g.esize < (int64_t(256) << 20)) return false;
+    const char* min_mb = std::getenv("TSR_CHUNK_MIN_MB");
+    const int64_t min_bytes = (min_mb ? std::atoll(min_mb) : 64) << 20;
+    if (!(env && *env == '1') && bytes < min_bytes) return false;
+    const char* mx = std::getenv("TSR_CHUNKS_MAX");
+    const int64_t max_chunks =
+        mx ? std::max(3, std::atoi(mx)) : (bytes < (int64_t(1) << 30) ? 16 : 32);
     Chunks c;
     c.ax = 3 - g.dims;
     c.n0 = g.n[c.ax];
@@ -456,7 +465,8 @@ bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     c.margin = steps * std::max(1, t.radius);
     // chunks of 2*T*r planes (windows twice the chunk): the first download
     // starts after a small share of the upload; at most 32 chunks
-    c.size = std::max<int64_t>({16, 2 * c.margin, (c.n0 + 31) / 32, 2 * c.h0 + 1});
+    c.size = std::max<int64_t>(
+        {16, 2 * c.margin, (c.n0 + max_chunks - 1) / max_chunks, 2 * c.h0 + 1});
     c.nchunks = static_cast<int>(c.n0 / c.size);  // the last chunk takes the remainder
     if (c.nchunks < 3) return false;
     c.hplane = g.hpitch[c.ax];
