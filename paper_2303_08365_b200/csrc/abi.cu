@@ -349,6 +349,8 @@ struct DeviceCache {
     std::vector<cudaEvent_t> pool;
     void* pipe = nullptr;
     int64_t pipe_bytes = 0;
+    void* hstage = nullptr;  // pinned host slots of the staged (pageable) round trip
+    int64_t hstage_bytes = 0;
 };
 std::mutex g_cache_mu;
 std::vector<DeviceCache> g_cache;
@@ -515,12 +517,12 @@ Status chunk_resources(const Geo& g, Chunks& ch, DeviceCache* c) {
 
 Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_opts& o,
                         DeviceCache* c, void* const host[2], int parity, int64_t steps,
-                        const Chunks& ch, tsr_stats* st);
+                        const Chunks& ch, tsr_stats* st, bool staged);
 
 Status run_chunked(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_opts& o,
                    DeviceCache* c, void* const host[2], int parity, int64_t steps,
-                   const Chunks& ch, tsr_stats* st) {
-    Status r = run_chunked_impl(gg, g, t, o, c, host, parity, steps, ch, st);
+                   const Chunks& ch, tsr_stats* st, bool staged) {
+    Status r = run_chunked_impl(gg, g, t, o, c, host, parity, steps, ch, st, staged);
     if (!r.ok()) {
         // nothing queued may still write the caller's host buffers
         cudaStreamSynchronize(c->s_out);
@@ -530,9 +532,60 @@ Status run_chunked(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_
     return r;
 }
 
+// memcpy over up to 8 host threads (pageable <-> pinned staging: one thread
+// copies ~10 GB/s, the driver's own pageable staging ~15 GB/s)
+void par_memcpy(void* dst, const void* src, int64_t n) {
+    const int nt = static_cast<int>(std::min<int64_t>(8, n / (4 << 20) + 1));
+    if (nt == 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const int64_t part = (n / nt + 63) / 64 * 64;
+    for (int i = 1; i < nt; ++i) {
+        const int64_t o = i * part;
+        if (o >= n) break;
+        th.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                        std::min(part, n - o));
+        });
+    }
+    std::memcpy(dst, src, std::min(part, n));
+    for (auto& x : th) x.join();
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// pinned host staging of the staged (pageable) round trip: NIN upload slots
+// of one piece, two sets of two download slots of the widest chunk
+constexpr int kInSlots = 3;
+Status host_stage_for(DeviceCache* c, int64_t bytes) {
+    if (c->hstage_bytes >= bytes) return Status::Ok();
+    if (c->hstage) cudaFreeHost(c->hstage);
+    c->hstage = nullptr;
+    c->hstage_bytes = 0;
+    TSR_CUDA_TRY(cudaHostAlloc(&c->hstage, bytes, cudaHostAllocDefault));
+    c->hstage_bytes = bytes;
+    return Status::Ok();
+}
+
+// The chunk loop of the chunked round trip.  Pinned host buffers: the upload
+// pieces are already queued (run_host) and every copy is a DMA straight
+// to/from the caller's buffers.  Pageable host buffers (STAGED): this thread
+// drives the pipeline — each piece is copied by host threads into a pinned
+// slot and DMA'd up, windows are queued as soon as their pieces are up, and
+// each finished chunk is DMA'd into a pinned slot and copied out by host
+// threads while later pieces go up.
 Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const tsr_opts& o,
                         DeviceCache* c, void* const host[2], int parity, int64_t steps,
-                        const Chunks& ch, tsr_stats* st) {
+                        const Chunks& ch, tsr_stats* st, bool staged) {
     // the whole grid's plan (engine, fused depth) for every window
     Plan p;
     Status r = plan_for(g, t, o, p);
@@ -546,32 +599,67 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
     cudaEvent_t* ev_rel = ev_c1 + ch.nchunks;
     cudaEvent_t* ev_out = ev_rel + ch.nchunks;
     const int pfinal = parity ^ static_cast<int>(steps & 1);
+    const int nout = steps >= 2 ? 2 : 1;
+    const int64_t hbytes = g.host_elements * es;
+    const int64_t pb = ch.piece * ch.hplane * es;   // bytes per upload piece
+    const int64_t ob = ch.out_elems * es;           // bytes per download slot
+    char* in_slot[kInSlots] = {};
+    char* out_slot[2][2] = {};
+    if (staged) {
+        r = host_stage_for(c, kInSlots * pb + 4 * ob);
+        if (!r.ok()) return r;
+        char* h = static_cast<char*>(c->hstage);
+        for (int i = 0; i < kInSlots; ++i) in_slot[i] = h + i * pb;
+        for (int s2 = 0; s2 < 2; ++s2)
+            for (int q = 0; q < 2; ++q) out_slot[s2][q] = h + kInSlots * pb + (2 * s2 + q) * ob;
+    }
+    auto chunk_span = [&](int j, int64_t* a, int64_t* b) {
+        *a = j * ch.size;
+        *b = j + 1 == ch.nchunks ? ch.n0 : *a + ch.size;
+    };
+    auto last_piece = [&](int j) {  // host planes [wa, wb + 2 h0) of window j
+        int64_t a, b;
+        chunk_span(j, &a, &b);
+        const int64_t wb = std::min(ch.n0, b + ch.margin);
+        return static_cast<int>((wb + 2 * ch.h0 - 1) / ch.piece);
+    };
     tsr_stats local{};
     int64_t d2h = 0;
-    for (int j = 0; j < ch.nchunks; ++j) {
+    int queued = 0, drained = 0;  // chunks queued / copied out (STAGED)
+    auto drain = [&](int j) -> Status {  // STAGED: chunk j's slots -> caller's buffers
+        int64_t a, b;
+        chunk_span(j, &a, &b);
+        TSR_CUDA_TRY(cudaEventSynchronize(ev_out[j]));
+        const int64_t n = (b - a) * ch.hplane * es, dst = (a + ch.h0) * ch.hplane * es;
+        for (int q = 0; q < nout; ++q)
+            par_memcpy(static_cast<char*>(host[q == 0 ? pfinal : 1 - pfinal]) + dst,
+                       out_slot[j & 1][q], n);
+        drained = j + 1;
+        return Status::Ok();
+    };
+    auto queue_chunk = [&](int j) -> Status {
         char* set = static_cast<char*>(c->pipe) + (j & 1) * (2 * ch.win_elems + 2 * ch.out_elems) * es;
         void* wbuf[2] = {set, set + ch.win_elems * es};
         char* ostage[2] = {set + 2 * ch.win_elems * es, set + (2 * ch.win_elems + ch.out_elems) * es};
-        const int64_t a = j * ch.size, b = j + 1 == ch.nchunks ? ch.n0 : a + ch.size;
+        int64_t a, b;
+        chunk_span(j, &a, &b);
         const int64_t wa = std::max<int64_t>(0, a - ch.margin);
         const int64_t wb = std::min(ch.n0, b + ch.margin);
         Geo gw;
-        r = make_geo(window_grid(gg, wb - wa), gw);
-        if (!r.ok()) return r;
-        // host planes [wa, wb + 2 h0) of the read buffer must have arrived
-        const int last_piece = static_cast<int>((wb + 2 * ch.h0 - 1) / ch.piece);
-        TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_comp, ev_in[last_piece], 0));
+        Status q0 = make_geo(window_grid(gg, wb - wa), gw);
+        if (!q0.ok()) return q0;
+        TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_comp, ev_in[last_piece(j)], 0));
         if (j >= 2) TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_comp, ev_out[j - 2], 0));
         TSR_CUDA_TRY(cudaEventRecord(ev_c0[j], c->s_comp));
-        r = relayout(gw, static_cast<const char*>(c->d[1]) + wa * ch.hplane * es, wbuf[0], true,
-                     c->s_comp);
-        if (!r.ok()) return r;
-        r = halo_copy(gw, wbuf[0], wbuf[1], c->s_comp);
-        if (!r.ok()) return r;
+        q0 = relayout(gw, static_cast<const char*>(c->d[1]) + wa * ch.hplane * es, wbuf[0], true,
+                      c->s_comp);
+        if (!q0.ok()) return q0;
+        q0 = halo_copy(gw, wbuf[0], wbuf[1], c->s_comp);
+        if (!q0.ok()) return q0;
         int cur = 0;
         tsr_stats ws{};
-        r = advance(gw, t, wo, wbuf[0], wbuf[1], &cur, steps, true, c->s_comp, &ws);
-        if (!r.ok()) return r;
+        q0 = advance(gw, t, wo, wbuf[0], wbuf[1], &cur, steps, true, c->s_comp, &ws);
+        if (!q0.ok()) return q0;
         TSR_CUDA_TRY(cudaEventRecord(ev_c1[j], c->s_comp));
         if (j == 0) {
             local.rounds = ws.rounds;
@@ -585,21 +673,63 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
         go.n[ch.ax] = b - a;
         go.h[ch.ax] = 0;
         const int64_t src_off = (a - wa + ch.h0) * gw.pitch[ch.ax] * es;
-        const int nout = steps >= 2 ? 2 : 1;
         for (int q = 0; q < nout; ++q) {
-            r = relayout(go, static_cast<const char*>(wbuf[q == 0 ? cur : 1 - cur]) + src_off,
-                         ostage[q], false, c->s_comp);
-            if (!r.ok()) return r;
+            q0 = relayout(go, static_cast<const char*>(wbuf[q == 0 ? cur : 1 - cur]) + src_off,
+                          ostage[q], false, c->s_comp);
+            if (!q0.ok()) return q0;
         }
         TSR_CUDA_TRY(cudaEventRecord(ev_rel[j], c->s_comp));
         TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_out, ev_rel[j], 0));
         const int64_t n = (b - a) * ch.hplane * es, dst = (a + ch.h0) * ch.hplane * es;
+        if (staged && j >= 2 && drained < j - 1) {
+            Status q1 = drain(j - 2);  // its pinned slots are this chunk's
+            if (!q1.ok()) return q1;
+        }
         for (int q = 0; q < nout; ++q) {
-            TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(host[q == 0 ? pfinal : 1 - pfinal]) + dst,
-                                         ostage[q], n, cudaMemcpyDeviceToHost, c->s_out));
+            void* to = staged ? static_cast<void*>(out_slot[j & 1][q])
+                              : static_cast<void*>(static_cast<char*>(
+                                    host[q == 0 ? pfinal : 1 - pfinal]) + dst);
+            TSR_CUDA_TRY(cudaMemcpyAsync(to, ostage[q], n, cudaMemcpyDeviceToHost, c->s_out));
             d2h += n;
         }
         TSR_CUDA_TRY(cudaEventRecord(ev_out[j], c->s_out));
+        queued = j + 1;
+        return Status::Ok();
+    };
+    if (!staged) {
+        for (int j = 0; j < ch.nchunks; ++j) {
+            r = queue_chunk(j);
+            if (!r.ok()) return r;
+        }
+    } else {
+        for (int i = 0; i < ch.npieces; ++i) {
+            // slot i % kInSlots is free once piece i - kInSlots is up
+            if (i >= kInSlots) TSR_CUDA_TRY(cudaEventSynchronize(ev_in[i - kInSlots]));
+            const int64_t off = i * pb, n = std::min(pb, hbytes - off);
+            char* sl = in_slot[i % kInSlots];
+            par_memcpy(sl, static_cast<const char*>(host[parity]) + off, n);
+            TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d[1]) + off, sl, n,
+                                         cudaMemcpyHostToDevice, c->stream));
+            TSR_CUDA_TRY(cudaEventRecord(ev_in[i], c->stream));
+            while (queued < ch.nchunks && last_piece(queued) <= i) {
+                r = queue_chunk(queued);
+                if (!r.ok()) return r;
+            }
+            // copy out whatever chunk has come down meanwhile
+            while (drained < queued && cudaEventQuery(ev_out[drained]) == cudaSuccess) {
+                r = drain(drained);
+                if (!r.ok()) return r;
+            }
+            cudaGetLastError();  // cudaErrorNotReady from the queries
+        }
+        while (queued < ch.nchunks) {
+            r = queue_chunk(queued);
+            if (!r.ok()) return r;
+        }
+        while (drained < ch.nchunks) {
+            r = drain(drained);
+            if (!r.ok()) return r;
+        }
     }
     const auto t_enq = std::chrono::steady_clock::now();
     TSR_CUDA_TRY(cudaStreamSynchronize(c->s_out));
@@ -616,22 +746,22 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
     if (const char* tr = std::getenv("TSR_CHUNK_TRACE"); tr && *tr == '1') {
         // per-window timeline (ms from the first upload piece's completion)
         for (int j = 0; j < ch.nchunks; ++j) {
-            float t[4] = {0, 0, 0, 0};
-            cudaEventElapsedTime(&t[0], ev_in[0], ev_c0[j]);
-            cudaEventElapsedTime(&t[1], ev_in[0], ev_c1[j]);
-            cudaEventElapsedTime(&t[2], ev_in[0], ev_rel[j]);
-            cudaEventElapsedTime(&t[3], ev_in[0], ev_out[j]);
+            float tt[4] = {0, 0, 0, 0};
+            cudaEventElapsedTime(&tt[0], ev_in[0], ev_c0[j]);
+            cudaEventElapsedTime(&tt[1], ev_in[0], ev_c1[j]);
+            cudaEventElapsedTime(&tt[2], ev_in[0], ev_rel[j]);
+            cudaEventElapsedTime(&tt[3], ev_in[0], ev_out[j]);
             std::fprintf(stderr, "chunk %d: start %.2f swept %.2f relaid %.2f downloaded %.2f\n", j,
-                         t[0], t[1], t[2], t[3]);
+                         tt[0], tt[1], tt[2], tt[3]);
         }
         float tl = 0;
         cudaEventElapsedTime(&tl, ev_in[0], ev_in[ch.npieces - 1]);
-        std::fprintf(stderr, "pieces %d, last piece uploaded %.2f; host waited %.2f ms\n",
-                     ch.npieces, tl, wait_ms);
+        std::fprintf(stderr, "pieces %d, last piece uploaded %.2f; host waited %.2f ms (staged=%d)\n",
+                     ch.npieces, tl, wait_ms, int(staged));
     }
     local.point_updates = g.interior() * steps;
     local.device_ms = ms;
-    local.h2d_bytes = g.host_elements * es;
+    local.h2d_bytes = hbytes;
     local.d2h_bytes = d2h;
     if (st) *st = local;
     return Status::Ok();
@@ -675,7 +805,10 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
         if (!r.ok()) return r;
         chunked = c->pipe != nullptr;
     }
-    if (chunked) {
+    // Pageable caller buffers: the chunked round trip stages its copies
+    // through pinned slots itself (run_chunked_impl) after the halo check.
+    const bool staged = chunked && !(is_pinned(b0) && is_pinned(b1));
+    if (chunked && !staged) {
         // the read buffer goes up in pieces, an event after each, so window
         // j computes as soon as the planes it reads have arrived
         const int64_t pb = ch.piece * ch.hplane * g.esize;
@@ -686,6 +819,8 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
                                          cudaMemcpyHostToDevice, c->stream));
             TSR_CUDA_TRY(cudaEventRecord(c->pool[i], c->stream));
         }
+    } else if (staged) {
+        // uploaded piece by piece in run_chunked_impl
     } else if (staged_up) {
         TSR_CUDA_TRY(cudaMemcpyAsync(c->d[1], host[parity], hbytes, cudaMemcpyHostToDevice,
                                      c->stream));
@@ -701,7 +836,12 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
         std::fprintf(stderr, "run_host: chunked=%d halo check %.2f ms\n", int(chunked),
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
                                                                t_enq).count());
-    if (chunked && same_halo) return run_chunked(*gg, g, t, o, c, host, parity, steps, ch, st);
+    if (chunked && same_halo)
+        return run_chunked(*gg, g, t, o, c, host, parity, steps, ch, st, staged);
+    if (staged) {  // differing halos: the whole read buffer after all
+        TSR_CUDA_TRY(cudaMemcpyAsync(c->d[1], host[parity], hbytes, cudaMemcpyHostToDevice,
+                                     c->stream));
+    }
     if (staged_up) {
         r = relayout(g, c->d[1], c->d[0], true, c->stream);
         if (!r.ok()) return r;
@@ -874,6 +1014,9 @@ int tsr_release_cache(void) {
         if (c.pipe) cudaFree(c.pipe);
         c.pipe = nullptr;
         c.pipe_bytes = 0;
+        if (c.hstage) cudaFreeHost(c.hstage);
+        c.hstage = nullptr;
+        c.hstage_bytes = 0;
         for (cudaEvent_t e : c.pool) cudaEventDestroy(e);
         c.pool.clear();
         if (c.s_comp) cudaStreamDestroy(c.s_comp), c.s_comp = nullptr;

@@ -546,16 +546,24 @@ def test_box27_separable_fast_within_tolerance(ts, orc, dt, fused):
     ("Heat-2D", "f64", [300, 90], "exact", None),
     ("Box-2D9P", "f64", [257, 130], "fast", None),
 ])
-def test_chunked_round_trip(ts, orc, monkeypatch, name, dt, extent, mode, halo):
+@pytest.mark.parametrize("pinned", [False, True])
+def test_chunked_round_trip(ts, orc, monkeypatch, name, dt, extent, mode, halo, pinned):
     """tsr_run's chunked round trip (short runs: chunks of the outermost axis
     advanced on windows widened by T*r planes, uploads, windows and downloads
     overlapped) returns exactly what the whole-grid round trip returns, and
     bitwise the oracle in EXACT mode: odd/even T, T = 1, parity 1, a
-    non-zero Dirichlet halo plane, chunk counts down to 3."""
+    non-zero Dirichlet halo plane, chunk counts down to 3; page-locked host
+    buffers (direct DMA) and pageable ones (copies staged through pinned
+    slots by host threads)."""
     k = ts.find_benchmark(name).kernel
 
     def grid(steps, parity):
         g = random_grid(ts, orc, extent, halo or [k.radius] * k.dims, 7, dt)
+        if pinned:
+            pg = type(g)(g.extent, g.halo, pinned=True)
+            for w in (0, 1):
+                pg.buffer(w)[:] = g.buffer(w)
+            g = pg
         for w in (0, 1):
             g.padded(w)[0] = 0.5
         if parity:
