@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
 #include <random>
 #include <sstream>
@@ -625,17 +626,43 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
     };
     tsr_stats local{};
     int64_t d2h = 0;
-    int queued = 0, drained = 0;  // chunks queued / copied out (STAGED)
-    auto drain = [&](int j) -> Status {  // STAGED: chunk j's slots -> caller's buffers
-        int64_t a, b;
-        chunk_span(j, &a, &b);
-        TSR_CUDA_TRY(cudaEventSynchronize(ev_out[j]));
-        const int64_t n = (b - a) * ch.hplane * es, dst = (a + ch.h0) * ch.hplane * es;
-        for (int q = 0; q < nout; ++q)
-            par_memcpy(static_cast<char*>(host[q == 0 ? pfinal : 1 - pfinal]) + dst,
-                       out_slot[j & 1][q], n);
-        drained = j + 1;
-        return Status::Ok();
+    // STAGED: a drainer thread copies each finished chunk out of its pinned
+    // slots while this thread copies pieces in and queues windows; `queued`
+    // (ev_out[j] recorded) and `drained` (slots of chunk j free) hand over.
+    std::mutex mu;
+    std::condition_variable cv;
+    int queued = 0, drained = 0;
+    bool stop = false;
+    Status drain_err;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto drainer = [&] {
+        cudaSetDevice(dev);
+        for (int j = 0; j < ch.nchunks; ++j) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return queued > j || stop; });
+                if (queued <= j) break;  // stopped
+            }
+            int64_t a, b;
+            chunk_span(j, &a, &b);
+            const cudaError_t e = cudaEventSynchronize(ev_out[j]);
+            if (e == cudaSuccess) {
+                const int64_t n = (b - a) * ch.hplane * es, dst = (a + ch.h0) * ch.hplane * es;
+                for (int q = 0; q < nout; ++q)
+                    par_memcpy(static_cast<char*>(host[q == 0 ? pfinal : 1 - pfinal]) + dst,
+                               out_slot[j & 1][q], n);
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            if (e != cudaSuccess) {
+                drain_err = Status::Err(TSR_ECUDA, cudaGetErrorString(e));
+                drained = ch.nchunks;  // unblock the queueing thread
+            } else {
+                drained = j + 1;
+            }
+            cv.notify_all();
+            if (e != cudaSuccess) break;
+        }
     };
     auto queue_chunk = [&](int j) -> Status {
         char* set = static_cast<char*>(c->pipe) + (j & 1) * (2 * ch.win_elems + 2 * ch.out_elems) * es;
@@ -681,9 +708,10 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
         TSR_CUDA_TRY(cudaEventRecord(ev_rel[j], c->s_comp));
         TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_out, ev_rel[j], 0));
         const int64_t n = (b - a) * ch.hplane * es, dst = (a + ch.h0) * ch.hplane * es;
-        if (staged && j >= 2 && drained < j - 1) {
-            Status q1 = drain(j - 2);  // its pinned slots are this chunk's
-            if (!q1.ok()) return q1;
+        if (staged && j >= 2) {  // chunk j-2's pinned slots are this chunk's
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return drained >= j - 1; });
+            if (!drain_err.ok()) return drain_err;
         }
         for (int q = 0; q < nout; ++q) {
             void* to = staged ? static_cast<void*>(out_slot[j & 1][q])
@@ -693,7 +721,11 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
             d2h += n;
         }
         TSR_CUDA_TRY(cudaEventRecord(ev_out[j], c->s_out));
-        queued = j + 1;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            queued = j + 1;
+        }
+        cv.notify_all();
         return Status::Ok();
     };
     if (!staged) {
@@ -702,34 +734,37 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
             if (!r.ok()) return r;
         }
     } else {
-        for (int i = 0; i < ch.npieces; ++i) {
-            // slot i % kInSlots is free once piece i - kInSlots is up
-            if (i >= kInSlots) TSR_CUDA_TRY(cudaEventSynchronize(ev_in[i - kInSlots]));
-            const int64_t off = i * pb, n = std::min(pb, hbytes - off);
-            char* sl = in_slot[i % kInSlots];
-            par_memcpy(sl, static_cast<const char*>(host[parity]) + off, n);
-            TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d[1]) + off, sl, n,
-                                         cudaMemcpyHostToDevice, c->stream));
-            TSR_CUDA_TRY(cudaEventRecord(ev_in[i], c->stream));
-            while (queued < ch.nchunks && last_piece(queued) <= i) {
-                r = queue_chunk(queued);
-                if (!r.ok()) return r;
+        std::thread th(drainer);
+        auto upload_and_queue = [&]() -> Status {
+            for (int i = 0; i < ch.npieces; ++i) {
+                // slot i % kInSlots is free once piece i - kInSlots is up
+                if (i >= kInSlots) TSR_CUDA_TRY(cudaEventSynchronize(ev_in[i - kInSlots]));
+                const int64_t off = i * pb, n = std::min(pb, hbytes - off);
+                char* sl = in_slot[i % kInSlots];
+                par_memcpy(sl, static_cast<const char*>(host[parity]) + off, n);
+                TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d[1]) + off, sl, n,
+                                             cudaMemcpyHostToDevice, c->stream));
+                TSR_CUDA_TRY(cudaEventRecord(ev_in[i], c->stream));
+                while (queued < ch.nchunks && last_piece(queued) <= i) {
+                    Status q = queue_chunk(queued);
+                    if (!q.ok()) return q;
+                }
             }
-            // copy out whatever chunk has come down meanwhile
-            while (drained < queued && cudaEventQuery(ev_out[drained]) == cudaSuccess) {
-                r = drain(drained);
-                if (!r.ok()) return r;
+            while (queued < ch.nchunks) {
+                Status q = queue_chunk(queued);
+                if (!q.ok()) return q;
             }
-            cudaGetLastError();  // cudaErrorNotReady from the queries
+            return Status::Ok();
+        };
+        r = upload_and_queue();
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;  // the drainer finishes the chunks queued so far
         }
-        while (queued < ch.nchunks) {
-            r = queue_chunk(queued);
-            if (!r.ok()) return r;
-        }
-        while (drained < ch.nchunks) {
-            r = drain(drained);
-            if (!r.ok()) return r;
-        }
+        cv.notify_all();
+        th.join();
+        if (!r.ok()) return r;
+        if (!drain_err.ok()) return drain_err;
     }
     const auto t_enq = std::chrono::steady_clock::now();
     TSR_CUDA_TRY(cudaStreamSynchronize(c->s_out));
