@@ -465,9 +465,10 @@ bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     c.ax = 3 - g.dims;
     c.n0 = g.n[c.ax];
     c.h0 = g.h[c.ax];
+    if (steps > c.n0) return false;  // the cone spans the axis (and T*r cannot overflow)
     c.margin = steps * std::max(1, t.radius);
     // chunks of 2*T*r planes (windows twice the chunk): the first download
-    // starts after a small share of the upload; at most 32 chunks
+    // starts after a small share of the upload; at most max_chunks of them
     c.size = std::max<int64_t>(
         {16, 2 * c.margin, (c.n0 + max_chunks - 1) / max_chunks, 2 * c.h0 + 1});
     c.nchunks = static_cast<int>(c.n0 / c.size);  // the last chunk takes the remainder
