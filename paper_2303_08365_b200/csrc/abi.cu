@@ -471,7 +471,9 @@ bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     // starts after a small share of the upload; at most max_chunks of them
     c.size = std::max<int64_t>(
         {16, 2 * c.margin, (c.n0 + max_chunks - 1) / max_chunks, 2 * c.h0 + 1});
-    c.nchunks = static_cast<int>(c.n0 / c.size);  // the last chunk takes the remainder
+    // n0 / size chunks of equal size (+-1 plane): no wide last chunk whose
+    // download would trail the others
+    c.nchunks = static_cast<int>(c.n0 / c.size);
     if (c.nchunks < 3) return false;
     c.hplane = g.hpitch[c.ax];
     c.piece = c.size;
@@ -499,7 +501,7 @@ Status chunk_resources(const Geo& g, Chunks& ch, DeviceCache* c) {
     }
     // window device buffers: the widest window's pitched layout (same row
     // pitch as the whole grid: only the plane count differs)
-    const int64_t last = ch.n0 - (ch.nchunks - 1) * ch.size;  // the widest chunk
+    const int64_t last = (ch.n0 + ch.nchunks - 1) / ch.nchunks;  // the widest chunk
     const int64_t wplanes = std::min(ch.n0, last + 2 * ch.margin);
     ch.win_elems = (wplanes + 2 * ch.h0) * g.pitch[ch.ax];
     ch.out_elems = last * ch.hplane;
@@ -616,8 +618,8 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
             for (int q = 0; q < 2; ++q) out_slot[s2][q] = h + kInSlots * pb + (2 * s2 + q) * ob;
     }
     auto chunk_span = [&](int j, int64_t* a, int64_t* b) {
-        *a = j * ch.size;
-        *b = j + 1 == ch.nchunks ? ch.n0 : *a + ch.size;
+        *a = j * ch.n0 / ch.nchunks;
+        *b = (j + 1) * ch.n0 / ch.nchunks;
     };
     auto last_piece = [&](int j) {  // host planes [wa, wb + 2 h0) of window j
         int64_t a, b;
