@@ -447,7 +447,8 @@ struct Chunks {
 bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     if (g.dims < 2) return false;
     // TSR_RUN_CHUNKED: 0 = never, 1 = whenever there are >= 3 chunks, unset =
-    // grids of >= 64 MiB per buffer (TSR_CHUNK_MIN_MB; below that the copies
+    // where the time model below predicts a gain, for grids of >= 64 MiB per
+    // buffer (TSR_CHUNK_MIN_MB; below that the copies
     // take a few ms and the extra launches cancel the overlap).  At most 16
     // chunks below 1 GiB per buffer, 32 above (TSR_CHUNKS_MAX), from a sweep
     // at T = 20 (tools/probe/chunk_sweep.py): 4096^2 fp64 7.8 -> 5.9 ms with
@@ -478,6 +479,24 @@ bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     c.hplane = g.hpitch[c.ax];
     c.piece = c.size;
     c.npieces = static_cast<int>((c.n0 + 2 * c.h0 + c.piece - 1) / c.piece);
+    if (!(env && *env == '1')) {
+        // Time model (seconds): copies at ~50 GB/s per direction, ~1.4x that
+        // with both directions busy; sweeps at a conservative 800 GS/s for
+        // fp64 (x 8/esize, x 9/taps beyond 9 taps); the windows sweep
+        // (size + 2 margin) / size times the points, and the first window
+        // waits for its planes.  Chunked only where it wins by >= 5%
+        // (measured crossover, tools/probe/chunk_T.py: 10000^2 Heat-2D
+        // T = 200 1.19x faster chunked, T = 400 0.86x).
+        const double up = double(bytes) / 50e9, down = (steps >= 2 ? 2 : 1) * up;
+        const double rate = 800e9 * (8.0 / g.esize) * std::min(1.0, 9.0 / std::max(1, t.ntaps));
+        const double sweep = double(g.interior()) * double(steps) / rate;
+        const double avg = double(c.n0) / c.nchunks;
+        const double f = (avg + 2.0 * double(c.margin)) / avg;
+        const double ramp = up * (avg + c.margin) / c.n0 + sweep * (avg + 2.0 * c.margin) / c.n0;
+        const double whole = up + sweep + down;
+        const double chunked = std::max((up + down) / 1.4, f * sweep) + ramp;
+        if (chunked > 0.95 * whole) return false;
+    }
     *ch = c;
     return true;
 }

@@ -110,7 +110,10 @@ __global__ void halo_copy_kernel(const T* __restrict__ src, T* __restrict__ dst,
     }
 }
 
-// One warp per padded row; `src`/`dst` rows start at r0*p0 + r1*p1 + off.
+// One warp per segment of up to kSeg elements of a padded row (a 1-D grid
+// is one row of 10^7 elements: one warp per row would copy it alone);
+// `src`/`dst` rows start at r0*p0 + r1*p1 + off.
+constexpr int64_t kSeg = 2048;
 template <typename T>
 __global__ void relayout_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t rows1,
                                 int64_t rows, int64_t width, int64_t sp0, int64_t sp1,
@@ -118,11 +121,14 @@ __global__ void relayout_kernel(const T* __restrict__ src, T* __restrict__ dst, 
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < rows; r += nwarps) {
+    const int64_t segs = (width + kSeg - 1) / kSeg;
+    for (int64_t w = warp; w < rows * segs; w += nwarps) {
+        const int64_t r = w / segs, x0 = (w - r * segs) * kSeg;
         const int64_t r0 = r / rows1, r1 = r - r0 * rows1;
         const T* s = src + r0 * sp0 + r1 * sp1 + soff;
         T* d = dst + r0 * dp0 + r1 * dp1 + doff;
-        for (int64_t x = lane; x < width; x += 32) d[x] = s[x];
+        const int64_t x1 = min(width, x0 + kSeg);
+        for (int64_t x = x0 + lane; x < x1; x += 32) d[x] = s[x];
     }
 }
 
@@ -130,7 +136,8 @@ template <typename T>
 void relayout_t(const Geo& g, const void* src, void* dst, bool h2d, cudaStream_t s) {
     const int64_t rows1 = g.n[1] + 2 * g.h[1], rows = g.rows_padded();
     const int64_t width = g.n[2] + 2 * g.h[2];
-    const int blocks = static_cast<int>(std::min<int64_t>((rows * 32 + 255) / 256, 148 * 16));
+    const int64_t items = rows * ((width + kSeg - 1) / kSeg);
+    const int blocks = static_cast<int>(std::min<int64_t>((items * 32 + 255) / 256, 148 * 16));
     const int64_t hp0 = g.hpitch[0], hp1 = g.hpitch[1], dp0 = g.pitch[0], dp1 = g.pitch[1];
     const int64_t doff = g.off2 - g.h[2];
     if (h2d)

@@ -339,13 +339,27 @@ bool classify(const TapSet& t, Shape* s) {
 constexpr int kMaxK = 8;
 constexpr int kMaxKBox2 = 2;  // 25-point box: five 6-wide rows per level in registers (k=3 spills)
 
+// Default fused depths from a k sweep over 4096^2, 9600^2 and 16384^2 fp64
+// (tools/probe_2d_k.py): k = 4 for the 5-point star and the 9-point box
+// (EXACT / Q mode: 919 at 16384^2 against 753-839 for k = 5..8), k = 3 for the
+// radius-2 star (its windows are 5 rows deep: 489 / 608 GS/s exact / fast at
+// 16384^2 against 468 / 584 at k = 4), and k = 5 for the 9-point box in FAST
+// (separable sums, fewer registers per level: 1156 against 1076 at 9600^2).
 bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
     Shape s;
     if (!classify(t, &s)) return false;
     const bool box2 = s.box && s.R == 2;
     *max_fused = box2 ? kMaxKBox2 : kMaxK;
-    *default_fused = box2 ? 2 : 4;
+    *default_fused = box2 ? 2 : (!s.box && s.R == 2) ? 3 : 4;
     return true;
+}
+
+int fast_default(const Geo& g, const TapSet& t) {
+    Shape s;
+    int maxk = 1, defk = 1;
+    if (!supports(g, t, &maxk, &defk)) return 1;
+    classify(t, &s);
+    return s.box && s.R == 1 && uniform_weights(t) ? 5 : defk;
 }
 
 template <typename T, int R, bool BOX, int K, int V>
@@ -451,6 +465,6 @@ Status run(const LaunchCtx& c, const void* in, void* out, int k) {
 
 }  // namespace
 
-extern const Engine kStream2dEngine = {"stream2d_regtile", supports, run};
+extern const Engine kStream2dEngine = {"stream2d_regtile", supports, run, fast_default};
 
 }  // namespace tsr

@@ -20,7 +20,8 @@ first verified at a reduced size, then timed at desk or full scale:
   reference's tolerance;
 * ``elapsed_s`` is the wall time of the reference-facing call (host buffers
   in and out, as the reference times execute_path); ``device_s`` is the CUDA
-  event time of the sweeps alone.
+  event time of the same steps run device-resident (DeviceGrid), the sweeps
+  alone.
 """
 from __future__ import annotations
 
@@ -134,6 +135,10 @@ def run_benchmark(name: str, path: str = "gpu", scale: str = "desk", threads: in
     warm = Grid(wext, [k.radius] * k.dims)
     run_gpu(warm, k, 2 * max(_fused(path, tb), 1) + 1, fused_steps=_fused(path, tb), mode=mode)
     g = Grid(extent, [k.radius] * k.dims, pinned=True)
+    if path != "hetero":
+        # and one untimed call of the timed size and length (device cache,
+        # chunked round-trip buffers), on the zero grid before it is seeded
+        run_gpu(g, k, t_steps, fused_steps=_fused(path, tb), mode=mode)
     fill_random(g, seed)
     if path == "hetero":
         t0 = time.perf_counter()
@@ -156,13 +161,36 @@ def run_benchmark(name: str, path: str = "gpu", scale: str = "desk", threads: in
     st = run_gpu(g, k, t_steps, fused_steps=_fused(path, tb), mode=mode)
     elapsed = max(time.perf_counter() - t0, 1e-9)
     rate = stencils_per_second(extent, t_steps, elapsed)
+    # device_s: the same steps device-resident (a short call's run_gpu may
+    # take the chunked round trip, whose windows sweep some planes twice)
+    dev_s = _device_seconds(g, k, t_steps, st.fused_steps, mode)
     row.update(elapsed_s=elapsed, stencils_per_s=rate.stencils_per_second, k=st.fused_steps,
-               device_s=st.device_ms / 1e3)
-    if st.device_ms > 0:
-        dev_rate = rate.points_per_step * t_steps / (st.device_ms / 1e3)
+               device_s=dev_s)
+    if dev_s > 0:
+        dev_rate = rate.points_per_step * t_steps / dev_s
         row["achieved_GBps"] = dev_rate * 2 * 8 / 1e9
         row["roofline_frac"] = row["achieved_GBps"] / _hbm_peak_gbps()
     return row
+
+
+def _device_seconds(g, k, steps, fused, mode) -> float:
+    """CUDA-event time of `steps` device-resident steps (DeviceGrid,
+    tsr_advance) of kernel `k` on grid `g`'s current state, after one
+    untimed launch."""
+    import torch  # plumbing: device buffers and events
+    from .device import DeviceGrid
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dg = DeviceGrid(g, dev)
+    dg.advance(k, max(1, fused), fused_steps=fused, mode=mode)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record()
+    dg.advance(k, steps, fused_steps=fused, mode=mode)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    del dg
+    return ms / 1e3
 
 
 CSV_FIELDS = ("name", "path", "dims", "extent", "T", "tile", "Tb", "elapsed_s",
