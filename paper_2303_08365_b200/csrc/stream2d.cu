@@ -343,14 +343,16 @@ constexpr int kMaxKBox2 = 2;  // 25-point box: five 6-wide rows per level in reg
 // (tools/probe_2d_k.py): k = 4 for the 5-point star and the 9-point box
 // (EXACT / Q mode: 919 at 16384^2 against 753-839 for k = 5..8), k = 3 for the
 // radius-2 star (its windows are 5 rows deep: 489 / 608 GS/s exact / fast at
-// 16384^2 against 468 / 584 at k = 4), and k = 5 for the 9-point box in FAST
-// (separable sums, fewer registers per level: 1156 against 1076 at 9600^2).
+// 16384^2 against 468 / 584 at k = 4), k = 1 for the 25-point box (10000^2:
+// 309 against 243 GS/s at k = 2, tools/probe/box25.py), and k = 5 for the
+// 9-point box in FAST (separable sums, fewer registers per level: 1156
+// against 1076 at 9600^2).
 bool supports(const Geo& g, const TapSet& t, int* max_fused, int* default_fused) {
     Shape s;
     if (!classify(t, &s)) return false;
     const bool box2 = s.box && s.R == 2;
     *max_fused = box2 ? kMaxKBox2 : kMaxK;
-    *default_fused = box2 ? 2 : (!s.box && s.R == 2) ? 3 : 4;
+    *default_fused = box2 ? 1 : (!s.box && s.R == 2) ? 3 : 4;
     return true;
 }
 
