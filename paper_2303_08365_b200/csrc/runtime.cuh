@@ -34,9 +34,16 @@ Status download(const Geo& g, const void* dev, void* host, bool interior_only, c
 // True when the halo shells of the two host buffers are bitwise equal.
 bool halos_equal(const Geo& g, const void* b0, const void* b1);
 
-// tsr_run on one device (the naive_run drop-in over host buffers).
+// `steps` time steps on device buffers d0/d1 (*cur = the read buffer, flipped
+// per launch); keep_prev leaves step T-1 in the other buffer (abi.cu).
+Status advance_grid(const Geo& g, const TapSet& t, const tsr_opts& o, void* d0, void* d1,
+                    int* cur, int64_t steps, bool keep_prev, cudaStream_t s, tsr_stats* st);
+
+// tsr_run on one device (the naive_run drop-in over host buffers), and the
+// release of the buffers it caches per device (roundtrip.cu).
 Status run_host_single(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b1, int parity,
                        int64_t steps, const tsr_opts* o, tsr_stats* st);
+void release_run_cache();
 
 // Sets the calling thread's device for a scope (and checks one exists).
 struct DeviceGuard {
