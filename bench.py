@@ -478,6 +478,40 @@ def pcie_bound(torch, dev, h2d_bytes, d2h_bytes, device_s, wall_s, updates):
                      "chunked round trip)"}
 
 
+def guarded(fn, what):
+    """Runs one optional leg of the line (e2e, cpu_baseline); a failure there
+    is reported in the line instead of losing the measured value."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001 - reported, not swallowed
+        import traceback
+        traceback.print_exc(file=sys.stderr)
+        return {"value": None, "error": f"{what}: {type(e).__name__}: {e}"[:300]}
+
+
+def single_e2e(ts, torch, cfg, k, per_gpu, kfused, mode, args, dev, elapsed_ms, points):
+    """The metric through run_gpu on pinned host buffers: one untimed call of
+    the same length sizes tsr_run's device cache, then the median of three
+    timed calls (each continues the last)."""
+    hg = make_grid(ts, cfg, per_gpu, pinned=True)
+    ts.run_gpu(hg, k, args.steps, fused_steps=kfused, mode=mode)
+    walls = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        st = ts.run_gpu(hg, k, args.steps, fused_steps=kfused, mode=mode)
+        walls.append(time.perf_counter() - t0)
+    wall = statistics.median(walls)
+    del hg
+    return {"value": round(points * args.steps / wall / 1e9, 3), "unit": "GStencil/s",
+            "h2d_bytes_per_step": round(st.h2d_bytes / args.steps, 1),
+            "d2h_bytes_per_step": round(st.d2h_bytes / args.steps, 1),
+            "call": "paper_2303_08365_b200.run_gpu(pinned Grid) -> tsr_run",
+            "wall_s": round(wall, 4), "walls_s": [round(w, 4) for w in walls],
+            "timing": "median of 3 calls after one untimed call of the same length",
+            "pcie": pcie_bound(torch, dev, st.h2d_bytes, st.d2h_bytes,
+                               elapsed_ms / 1e3, wall, points * args.steps)}
+
+
 def run_single(args, cfg):
     """N = 1: DeviceGrid (tsr_advance) on cuda:0, CUDA events per fused pass."""
     import torch
@@ -551,31 +585,14 @@ def run_single(args, cfg):
 
     modes = None
     if not args.no_mode_check:
-        modes = mode_check(ts, torch, cfg, k, host, state, per_gpu, dev, stream, kfused, mode,
-                           args, points, elapsed_ms)
+        modes = guarded(lambda: mode_check(ts, torch, cfg, k, host, state, per_gpu, dev, stream,
+                                           kfused, mode, args, points, elapsed_ms), "modes")
     del state
     e2e = None
     if not args.no_e2e:
-        hg = make_grid(ts, cfg, per_gpu, pinned=True)
-        # one untimed call of the same length sizes tsr_run's device cache,
-        # then the median of three timed calls (each continues the last)
-        ts.run_gpu(hg, k, args.steps, fused_steps=kfused, mode=mode)
-        walls = []
-        for _ in range(3):
-            t0 = time.perf_counter()
-            st = ts.run_gpu(hg, k, args.steps, fused_steps=kfused, mode=mode)
-            walls.append(time.perf_counter() - t0)
-        wall = statistics.median(walls)
-        e2e = {"value": round(points * args.steps / wall / 1e9, 3), "unit": "GStencil/s",
-               "h2d_bytes_per_step": round(st.h2d_bytes / args.steps, 1),
-               "d2h_bytes_per_step": round(st.d2h_bytes / args.steps, 1),
-               "call": "paper_2303_08365_b200.run_gpu(pinned Grid) -> tsr_run",
-               "wall_s": round(wall, 4), "walls_s": [round(w, 4) for w in walls],
-               "timing": "median of 3 calls after one untimed call of the same length",
-               "pcie": pcie_bound(torch, dev, st.h2d_bytes, st.d2h_bytes,
-                                  elapsed_ms / 1e3, wall, points * args.steps)}
-        del hg
-    cpu = None if args.no_cpu else cpu_baseline(cfg, 1)
+        e2e = guarded(lambda: single_e2e(ts, torch, cfg, k, per_gpu, kfused, mode, args, dev,
+                                         elapsed_ms, points), "e2e")
+    cpu = None if args.no_cpu else guarded(lambda: cpu_baseline(cfg, 1), "cpu_baseline")
     line = base_line(args, cfg, 1, mode, value, elapsed_ms)
     line.update({"plan": {"fused_steps": kfused,
                           "engine": {1: "generic", 2: "tuned"}.get(engine, str(engine)),
@@ -631,24 +648,33 @@ def run_slabs(args, cfg, n):
     e2e = None
     host_bytes = 2 * esize * npoints([g + 2 for g in glob])
     if not args.no_e2e and host_bytes <= args.e2e_host_limit_gb * 1e9:
-        hg = make_grid(ts, cfg, glob, pinned=True)
-        ts.run_multi(hg, k, min(2, args.steps), n, devices=devices, fused_steps=kfused,
-                     mode=mode)  # warm (slab allocation, kernel load)
-        ts.fill_random(hg, 1)
-        t0 = time.perf_counter()
-        st2 = ts.run_multi(hg, k, args.steps, n, devices=devices, fused_steps=kfused, mode=mode)
-        wall = time.perf_counter() - t0
-        e2e = {"value": round(points_glob * args.steps / wall / 1e9, 3), "unit": "GStencil/s",
-               "h2d_bytes_per_step": round(st2.h2d_bytes / args.steps, 1),
-               "d2h_bytes_per_step": round(st2.d2h_bytes / args.steps, 1),
-               "call": f"paper_2303_08365_b200.run_multi(pinned Grid, ngpus={n}) -> "
-                       "tsr_run_multi", "wall_s": round(wall, 4)}
-        del hg
-        ts.release_cache()
+        def multi_e2e():
+            hg = make_grid(ts, cfg, glob, pinned=True)
+            # one untimed call of the same length (slab allocation, kernel
+            # load), then the median of three timed calls
+            ts.run_multi(hg, k, args.steps, n, devices=devices, fused_steps=kfused, mode=mode)
+            walls = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                st2 = ts.run_multi(hg, k, args.steps, n, devices=devices, fused_steps=kfused,
+                                   mode=mode)
+                walls.append(time.perf_counter() - t0)
+            wall = statistics.median(walls)
+            del hg
+            ts.release_cache()
+            return {"value": round(points_glob * args.steps / wall / 1e9, 3),
+                    "unit": "GStencil/s",
+                    "h2d_bytes_per_step": round(st2.h2d_bytes / args.steps, 1),
+                    "d2h_bytes_per_step": round(st2.d2h_bytes / args.steps, 1),
+                    "call": f"paper_2303_08365_b200.run_multi(pinned Grid, ngpus={n}) -> "
+                            "tsr_run_multi", "wall_s": round(wall, 4),
+                    "walls_s": [round(w, 4) for w in walls],
+                    "timing": "median of 3 calls after one untimed call of the same length"}
+        e2e = guarded(multi_e2e, "e2e")
     elif not args.no_e2e:
         e2e = {"value": None, "skipped": f"global host grid {host_bytes / 1e9:.1f} GB exceeds "
                                          f"--e2e-host-limit-gb {args.e2e_host_limit_gb}"}
-    cpu = None if args.no_cpu else cpu_baseline(cfg, n)
+    cpu = None if args.no_cpu else guarded(lambda: cpu_baseline(cfg, n), "cpu_baseline")
     line = base_line(args, cfg, n, mode, value, elapsed_ms)
     line.update({"plan": {"fused_steps": kfused, "engine": "tuned", "runtime":
                           "one host thread, tsr_multi (csrc/multi.cu)"},
