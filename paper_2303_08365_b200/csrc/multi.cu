@@ -22,10 +22,12 @@
 //     for its own interior pass of round n-1; its interior pass of round n
 //     waits for its own seam pass of round n-1.
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
 #include <functional>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <random>
 #include <string>
 #include <vector>
@@ -725,6 +727,122 @@ bool cache_matches(const Multi* m, const Geo& g, const TapSet& t, const tsr_opts
            m->key_transport == transport && m->key_flags == flags;
 }
 
+// Short runs (T*r small against each slab) need no exchange at all: each
+// device computes its slab's planes of steps T and T-1 through the chunked
+// round trip (run_host_range), its windows reading the T*r planes beyond the
+// slab from the host buffers — replicated ghost zones, the seam work done
+// twice instead of exchanged.  One host thread per device (slabs sharing a
+// device run one after the other); TSR_EUNSUPPORTED when a slab is too
+// short for the chunked round trip, and the slab runtime runs instead.
+Status run_split(const tsr_kernel* kk, const tsr_grid* gg, const Geo& g, void* b0, void* b1,
+                 int parity, int64_t steps, const tsr_partition* part, const tsr_opts& o, int P,
+                 tsr_stats* st) {
+    if (g.dims < 2) return Status::Err(TSR_EUNSUPPORTED, "1-D grid");
+    if ((part ? part->split_axis : o.split_axis) != 0)
+        return Status::Err(TSR_EUNSUPPORTED, "split axis");
+    if (const char* e = std::getenv("TSR_MULTI_SPLIT"); e && *e == '0')
+        return Status::Err(TSR_EUNSUPPORTED, "disabled");
+    const int64_t n = g.n[3 - g.dims];
+    if (P > n) return Status::Err(TSR_EUNSUPPORTED, "more slabs than planes");
+    std::vector<int64_t> lo(P), hi(P);
+    for (int i = 0; i < P; ++i) {
+        if (part && part->boundaries) {
+            lo[i] = i == 0 ? 0 : part->boundaries[i - 1];
+            hi[i] = i == P - 1 ? n : part->boundaries[i];
+        } else {
+            const int64_t base = n / P, extra = n % P;
+            lo[i] = i * base + std::min<int64_t>(i, extra);
+            hi[i] = lo[i] + base + (i < extra ? 1 : 0);
+        }
+        if (lo[i] >= hi[i]) return Status::Err(TSR_EUNSUPPORTED, "empty slab");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return Status::Err(TSR_ECUDA, "no CUDA device available to the B200 sweep engine");
+    }
+    std::vector<int> dev(P);
+    for (int i = 0; i < P; ++i) dev[i] = part && part->devices ? part->devices[i] : i % ndev;
+    // One plane range per device: its slabs must be consecutive (round-robin
+    // placement on fewer devices than slabs is not), merged into one range.
+    // (TSR_SPLIT_PER_SLAB=1 keeps one range per slab, each with buffers of
+    // its own: the barrier across ranges can then run on a single device.)
+    const char* per = std::getenv("TSR_SPLIT_PER_SLAB");
+    const bool per_slab = per && *per == '1';
+    std::vector<int> rdev, rsub;
+    std::vector<int64_t> rlo, rhi;
+    for (int i = 0; i < P; ++i) {
+        if (!per_slab && !rdev.empty() && rdev.back() == dev[i]) {
+            rhi.back() = hi[i];
+            continue;
+        }
+        const int prior = static_cast<int>(std::count(rdev.begin(), rdev.end(), dev[i]));
+        if (prior > 0 && !per_slab)
+            return Status::Err(TSR_EUNSUPPORTED, "a device's slabs are not consecutive");
+        rdev.push_back(dev[i]);
+        rsub.push_back(prior);
+        rlo.push_back(lo[i]);
+        rhi.push_back(hi[i]);
+    }
+    const int D = static_cast<int>(rdev.size());
+    // every range must take the chunked round trip (checked before any
+    // buffer is written; else the slab runtime runs the whole call)
+    TapSet t;
+    Status r = make_taps(*kk, t);
+    if (!r.ok()) return r;
+    for (int i = 0; i < D; ++i)
+        if (!range_chunkable(g, t, steps, rlo[i], rhi[i]))
+            return Status::Err(TSR_EUNSUPPORTED, "slab too short for the chunked round trip");
+    // Barrier: every device has its margin planes up before any device
+    // writes planes back into the host buffers.  A device that fails before
+    // the barrier still arrives, so the others do not wait forever.
+    std::mutex bm;
+    std::condition_variable bcv;
+    int arrived = 0;
+    auto arrive = [&](bool wait) {
+        std::unique_lock<std::mutex> lk(bm);
+        ++arrived;
+        bcv.notify_all();
+        if (wait) bcv.wait(lk, [&] { return arrived >= D; });
+    };
+    std::vector<Status> res(D);
+    std::vector<tsr_stats> sts(D);
+    std::vector<std::thread> th;
+    for (int i = 0; i < D; ++i)
+        th.emplace_back([&, i] {
+            bool did = false;
+            const std::function<void()> cb = [&] {
+                did = true;
+                arrive(true);
+            };
+            tsr_opts od = o;
+            od.ngpus = 1;
+            od.device = rdev[i];
+            res[i] = run_host_range(kk, gg, b0, b1, parity, steps, &od, &sts[i], rlo[i], rhi[i], cb,
+                                    rsub[i]);
+            if (!did) arrive(false);
+        });
+    for (auto& x : th) x.join();
+    for (int i = 0; i < D; ++i)
+        if (!res[i].ok())
+            return res[i].code == TSR_EUNSUPPORTED ? Status::Err(TSR_ECUDA, res[i].msg) : res[i];
+    tsr_stats out{};
+    for (int i = 0; i < D; ++i) {
+        out.point_updates += sts[i].point_updates;
+        out.kernel_launches += sts[i].kernel_launches;
+        out.h2d_bytes += sts[i].h2d_bytes;
+        out.d2h_bytes += sts[i].d2h_bytes;
+        out.device_ms = std::max(out.device_ms, sts[i].device_ms);
+    }
+    out.rounds = sts[0].rounds;
+    out.trailing_steps = sts[0].trailing_steps;
+    out.fused_steps = sts[0].fused_steps;
+    out.engine = sts[0].engine;
+    out.ngpus = P;
+    if (st) *st = out;
+    return Status::Ok();
+}
+
 Status run_multi(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, int parity,
                  int64_t steps, const tsr_partition* part, bool keep_prev, const tsr_opts* oo,
                  tsr_stats* st) {
@@ -757,6 +875,11 @@ Status run_multi(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, i
     if (!r.ok()) return r;
 
     const int P = part ? part->ngpus : std::max(1, o.ngpus);
+    if (keep_prev && P > 1) {
+        r = run_split(kk, gg, g, b0, b1, parity, steps, part, o, P, st);
+        if (r.code != TSR_EUNSUPPORTED) return r;
+        cudaGetLastError();
+    }
     std::vector<int32_t> devs;
     std::vector<int64_t> bounds;
     if (part && part->devices) devs.assign(part->devices, part->devices + P);

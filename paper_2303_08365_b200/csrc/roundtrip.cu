@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -39,13 +41,30 @@ struct DeviceCache {
     int64_t pipe_bytes = 0;
     void* hstage = nullptr;  // pinned host slots of the staged (pageable) round trip
     int64_t hstage_bytes = 0;
+    std::mutex mu;  // held by the call using this device's cache
+    int device = 0;
 };
-std::mutex g_cache_mu;
-std::vector<DeviceCache> g_cache;
+std::mutex g_cache_mu;  // guards g_cache itself
+std::vector<std::unique_ptr<DeviceCache>> g_cache;
 
-Status cache_for(int dev, int64_t bytes, DeviceCache** out) {
-    if (static_cast<int>(g_cache.size()) <= dev) g_cache.resize(dev + 1);
-    DeviceCache& c = g_cache[dev];
+// Cache `sub` of device `dev` (sub > 0: a second range of tsr_run_multi's
+// split round trip on the same device, which needs buffers of its own).
+constexpr int kSubs = 16;
+DeviceCache* cache_slot(int dev, int sub = 0) {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    const size_t key = static_cast<size_t>(dev) * kSubs + sub % kSubs;
+    if (g_cache.size() <= key) g_cache.resize(key + 1);
+    if (!g_cache[key]) {
+        g_cache[key] = std::make_unique<DeviceCache>();
+        g_cache[key]->device = dev;
+    }
+    return g_cache[key].get();
+}
+
+// Streams, events and the two work buffers of device `dev`'s cache (the
+// caller holds its mutex).
+Status cache_for(DeviceCache* slot, int64_t bytes, DeviceCache** out) {
+    DeviceCache& c = *slot;
     if (!c.stream) {
         TSR_CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         TSR_CUDA_TRY(cudaEventCreate(&c.ev[0]));
@@ -95,9 +114,21 @@ struct Chunks {
     int npieces = 0;
     int64_t hplane = 0;   // host elements per plane
     int64_t win_elems = 0, out_elems = 0;  // per buffer of one window set
+    int64_t r_lo = 0, r_hi = 0;            // the planes this call returns
+    int piece_lo = 0, piece_hi = 0;        // the pieces its windows read
+    // split round trip (tsr_run_multi): the pieces holding planes outside
+    // [r_lo, r_hi) go up first, before any device writes its planes back
+    bool margins_first = false;
+    bool pre(int i) const {
+        const int64_t a = i * piece, b = a + piece;
+        return margins_first && !(a >= r_lo + h0 && b <= r_hi + h0);
+    }
 };
 
-bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
+// Chunks over the interior planes [r_lo, r_hi) of the outermost axis (the
+// whole axis for tsr_run; one device's share for tsr_run_multi's short runs).
+bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, int64_t r_lo, int64_t r_hi,
+                 Chunks* ch) {
     if (g.dims < 2) return false;
     // TSR_RUN_CHUNKED: 0 = never, 1 = whenever there are >= 3 chunks, unset =
     // where the time model below predicts a gain, for grids of >= 64 MiB per
@@ -106,7 +137,8 @@ bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     // chunks below 1 GiB per buffer, 32 above (TSR_CHUNKS_MAX), from a sweep
     // at T = 20 (tools/probe/chunk_sweep.py): 4096^2 fp64 7.8 -> 5.9 ms with
     // 16 (7.1 with 32), 16384^2 121.6 -> 84.2 ms with 32 (85.8 with 16).
-    const int64_t bytes = g.host_elements * g.esize;
+    const int64_t n_all = g.n[3 - g.dims];
+    const int64_t bytes = g.host_elements * g.esize * (r_hi - r_lo) / std::max<int64_t>(1, n_all);
     const char* env = std::getenv("TSR_RUN_CHUNKED");
     if (env && *env == '0') return false;
     const char* min_mb = std::getenv("TSR_CHUNK_MIN_MB");
@@ -119,19 +151,25 @@ bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
     c.ax = 3 - g.dims;
     c.n0 = g.n[c.ax];
     c.h0 = g.h[c.ax];
-    if (steps > c.n0) return false;  // the cone spans the axis (and T*r cannot overflow)
+    c.r_lo = r_lo;
+    c.r_hi = r_hi;
+    const int64_t n = r_hi - r_lo;
+    if (steps > n) return false;  // the cone spans the range (and T*r cannot overflow)
     c.margin = steps * std::max(1, t.radius);
     // chunks of 2*T*r planes (windows twice the chunk): the first download
     // starts after a small share of the upload; at most max_chunks of them
     c.size = std::max<int64_t>(
-        {16, 2 * c.margin, (c.n0 + max_chunks - 1) / max_chunks, 2 * c.h0 + 1});
-    // n0 / size chunks of equal size (+-1 plane): no wide last chunk whose
+        {16, 2 * c.margin, (n + max_chunks - 1) / max_chunks, 2 * c.h0 + 1});
+    // n / size chunks of equal size (+-1 plane): no wide last chunk whose
     // download would trail the others
-    c.nchunks = static_cast<int>(c.n0 / c.size);
+    c.nchunks = static_cast<int>(n / c.size);
     if (c.nchunks < 3) return false;
     c.hplane = g.hpitch[c.ax];
     c.piece = c.size;
     c.npieces = static_cast<int>((c.n0 + 2 * c.h0 + c.piece - 1) / c.piece);
+    // host planes [max(0, r_lo - margin), min(n0, r_hi + margin) + 2 h0)
+    c.piece_lo = static_cast<int>(std::max<int64_t>(0, r_lo - c.margin) / c.piece);
+    c.piece_hi = static_cast<int>((std::min(c.n0, r_hi + c.margin) + 2 * c.h0 - 1) / c.piece);
     if (!(env && *env == '1')) {
         // Time model (seconds): copies at ~50 GB/s per direction, ~1.4x that
         // with both directions busy; sweeps at a conservative 800 GS/s for
@@ -142,10 +180,10 @@ bool plan_chunks(const Geo& g, const TapSet& t, int64_t steps, Chunks* ch) {
         // T = 200 1.19x faster chunked, T = 400 0.86x).
         const double up = double(bytes) / 50e9, down = (steps >= 2 ? 2 : 1) * up;
         const double rate = 800e9 * (8.0 / g.esize) * std::min(1.0, 9.0 / std::max(1, t.ntaps));
-        const double sweep = double(g.interior()) * double(steps) / rate;
-        const double avg = double(c.n0) / c.nchunks;
+        const double sweep = double(g.interior()) * double(n) / double(c.n0) * double(steps) / rate;
+        const double avg = double(n) / c.nchunks;
         const double f = (avg + 2.0 * double(c.margin)) / avg;
-        const double ramp = up * (avg + c.margin) / c.n0 + sweep * (avg + 2.0 * c.margin) / c.n0;
+        const double ramp = up * (avg + c.margin) / n + sweep * (avg + 2.0 * c.margin) / n;
         const double whole = up + sweep + down;
         const double chunked = std::max((up + down) / 1.4, f * sweep) + ramp;
         if (chunked > 0.95 * whole) return false;
@@ -173,7 +211,7 @@ Status chunk_resources(const Geo& g, Chunks& ch, DeviceCache* c) {
     }
     // window device buffers: the widest window's pitched layout (same row
     // pitch as the whole grid: only the plane count differs)
-    const int64_t last = (ch.n0 + ch.nchunks - 1) / ch.nchunks;  // the widest chunk
+    const int64_t last = (ch.r_hi - ch.r_lo + ch.nchunks - 1) / ch.nchunks;  // the widest chunk
     const int64_t wplanes = std::min(ch.n0, last + 2 * ch.margin);
     ch.win_elems = (wplanes + 2 * ch.h0) * g.pitch[ch.ax];
     ch.out_elems = last * ch.hplane;
@@ -290,8 +328,9 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
             for (int q = 0; q < 2; ++q) out_slot[s2][q] = h + kInSlots * pb + (2 * s2 + q) * ob;
     }
     auto chunk_span = [&](int j, int64_t* a, int64_t* b) {
-        *a = j * ch.n0 / ch.nchunks;
-        *b = (j + 1) * ch.n0 / ch.nchunks;
+        const int64_t n = ch.r_hi - ch.r_lo;
+        *a = ch.r_lo + j * n / ch.nchunks;
+        *b = ch.r_lo + (j + 1) * n / ch.nchunks;
     };
     auto last_piece = [&](int j) {  // host planes [wa, wb + 2 h0) of window j
         int64_t a, b;
@@ -350,7 +389,12 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
         Geo gw;
         Status q0 = make_geo(window_grid(gg, wb - wa), gw);
         if (!q0.ok()) return q0;
-        TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_comp, ev_in[last_piece(j)], 0));
+        // pieces go up in index order on one stream, so the event of the
+        // window's last piece covers the ones before it; pieces that went up
+        // before the margins barrier have arrived already
+        int lp = last_piece(j);
+        while (lp >= ch.piece_lo && ch.pre(lp)) --lp;
+        if (lp >= ch.piece_lo) TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_comp, ev_in[lp], 0));
         if (j >= 2) TSR_CUDA_TRY(cudaStreamWaitEvent(c->s_comp, ev_out[j - 2], 0));
         TSR_CUDA_TRY(cudaEventRecord(ev_c0[j], c->s_comp));
         q0 = relayout(gw, static_cast<const char*>(c->d[1]) + wa * ch.hplane * es, wbuf[0], true,
@@ -410,12 +454,23 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
         }
     } else {
         std::thread th(drainer);
+        int slot_owner[kInSlots];
+        for (int& x : slot_owner) x = -1;
         auto upload_and_queue = [&]() -> Status {
-            for (int i = 0; i < ch.npieces; ++i) {
-                // slot i % kInSlots is free once piece i - kInSlots is up
-                if (i >= kInSlots) TSR_CUDA_TRY(cudaEventSynchronize(ev_in[i - kInSlots]));
+            for (int i = ch.piece_lo; i <= ch.piece_hi; ++i) {
+                if (ch.pre(i)) {  // uploaded before the margins barrier
+                    while (queued < ch.nchunks && last_piece(queued) <= i) {
+                        Status q = queue_chunk(queued);
+                        if (!q.ok()) return q;
+                    }
+                    continue;
+                }
+                // a slot is free once the piece last copied through it is up
+                const int si = (i - ch.piece_lo) % kInSlots;
+                if (slot_owner[si] >= 0) TSR_CUDA_TRY(cudaEventSynchronize(ev_in[slot_owner[si]]));
+                slot_owner[si] = i;
                 const int64_t off = i * pb, n = std::min(pb, hbytes - off);
-                char* sl = in_slot[i % kInSlots];
+                char* sl = in_slot[si];
                 par_memcpy(sl, static_cast<const char*>(host[parity]) + off, n);
                 TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d[1]) + off, sl, n,
                                              cudaMemcpyHostToDevice, c->stream));
@@ -457,28 +512,34 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
         // per-window timeline (ms from the first upload piece's completion)
         for (int j = 0; j < ch.nchunks; ++j) {
             float tt[4] = {0, 0, 0, 0};
-            cudaEventElapsedTime(&tt[0], ev_in[0], ev_c0[j]);
-            cudaEventElapsedTime(&tt[1], ev_in[0], ev_c1[j]);
-            cudaEventElapsedTime(&tt[2], ev_in[0], ev_rel[j]);
-            cudaEventElapsedTime(&tt[3], ev_in[0], ev_out[j]);
+            cudaEventElapsedTime(&tt[0], ev_in[ch.piece_lo], ev_c0[j]);
+            cudaEventElapsedTime(&tt[1], ev_in[ch.piece_lo], ev_c1[j]);
+            cudaEventElapsedTime(&tt[2], ev_in[ch.piece_lo], ev_rel[j]);
+            cudaEventElapsedTime(&tt[3], ev_in[ch.piece_lo], ev_out[j]);
             std::fprintf(stderr, "chunk %d: start %.2f swept %.2f relaid %.2f downloaded %.2f\n", j,
                          tt[0], tt[1], tt[2], tt[3]);
         }
         float tl = 0;
-        cudaEventElapsedTime(&tl, ev_in[0], ev_in[ch.npieces - 1]);
+        cudaEventElapsedTime(&tl, ev_in[ch.piece_lo], ev_in[ch.piece_hi]);
         std::fprintf(stderr, "pieces %d, last piece uploaded %.2f; host waited %.2f ms (staged=%d)\n",
                      ch.npieces, tl, wait_ms, int(staged));
     }
-    local.point_updates = g.interior() * steps;
+    local.point_updates = g.interior() / ch.n0 * (ch.r_hi - ch.r_lo) * steps;
     local.device_ms = ms;
-    local.h2d_bytes = hbytes;
+    local.h2d_bytes = std::min(hbytes, (int64_t(ch.piece_hi) + 1) * pb) - int64_t(ch.piece_lo) * pb;
     local.d2h_bytes = d2h;
     if (st) *st = local;
     return Status::Ok();
 }
 
+// With a plane range [r_lo, r_hi) of the outermost axis (r_hi >= 0), only
+// those planes of the two buffers are computed and returned, through the
+// chunked round trip (TSR_EUNSUPPORTED when it does not apply); the windows
+// read the planes they need beyond the range from the host buffers.
 Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, int parity,
-                int64_t steps, const tsr_opts* oo, tsr_stats* st) {
+                int64_t steps, const tsr_opts* oo, tsr_stats* st, int64_t r_lo = 0,
+                int64_t r_hi = -1, const std::function<void()>* after_margins = nullptr,
+                int cache_sub = 0) {
     if (!kk || !gg || !b0 || !b1) return Status::Err(TSR_EINVAL, "null argument");
     if (parity != 0 && parity != 1) return Status::Err(TSR_EINVAL, "parity must be 0 or 1");
     if (steps < 0) return Status::Err(TSR_EINVAL, "negative step count");
@@ -498,9 +559,10 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     if (!r.ok()) return r;
     int dev = 0;
     TSR_CUDA_TRY(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lock(g_cache_mu);
+    DeviceCache* slot = cache_slot(dev, cache_sub);
+    std::lock_guard<std::mutex> lock(slot->mu);
     DeviceCache* c = nullptr;
-    r = cache_for(dev, g.elements * g.esize, &c);
+    r = cache_for(slot, g.elements * g.esize, &c);
     if (!r.ok()) return r;
     void* host[2] = {b0, b1};
     // PCIe moves one contiguous block per buffer; the pitched device layout
@@ -509,11 +571,36 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
     const int64_t hbytes = g.host_elements * g.esize;
     const bool staged_up = c->bytes >= hbytes;  // d[1] can hold the host layout
     Chunks ch;
-    bool chunked = staged_up && plan_chunks(g, t, steps, &ch);
+    const int64_t n_all = g.n[3 - g.dims];
+    const bool partial = r_hi >= 0 && !(r_lo == 0 && r_hi == n_all);
+    if (r_hi < 0) r_hi = n_all;
+    if (r_lo < 0 || r_hi > n_all || r_lo >= r_hi)
+        return Status::Err(TSR_EINVAL, "plane range outside the grid");
+    bool chunked = staged_up && plan_chunks(g, t, steps, r_lo, r_hi, &ch);
     if (chunked) {
         r = chunk_resources(g, ch, c);
         if (!r.ok()) return r;
         chunked = c->pipe != nullptr;
+    }
+    if (partial && !chunked)
+        return Status::Err(TSR_EUNSUPPORTED, "plane range without the chunked round trip");
+    if (chunked && after_margins) {
+        // Split round trip: every other device writes its planes of steps T
+        // and T-1 back into these host buffers, the read buffer included, so
+        // the planes this range's windows read beyond it go up (and arrive)
+        // before any device downloads; then the pipeline as usual.
+        ch.margins_first = true;
+        const int64_t pb = ch.piece * ch.hplane * g.esize;
+        for (int i = ch.piece_lo; i <= ch.piece_hi; ++i) {
+            if (!ch.pre(i)) continue;
+            const int64_t off = i * pb, n = std::min(pb, hbytes - off);
+            TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d[1]) + off,
+                                         static_cast<const char*>(host[parity]) + off, n,
+                                         cudaMemcpyHostToDevice, c->stream));
+            TSR_CUDA_TRY(cudaEventRecord(c->pool[i], c->stream));
+        }
+        TSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        (*after_margins)();
     }
     // Pageable caller buffers: the chunked round trip stages its copies
     // through pinned slots itself (run_chunked_impl) after the halo check.
@@ -522,7 +609,8 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
         // the read buffer goes up in pieces, an event after each, so window
         // j computes as soon as the planes it reads have arrived
         const int64_t pb = ch.piece * ch.hplane * g.esize;
-        for (int i = 0; i < ch.npieces; ++i) {
+        for (int i = ch.piece_lo; i <= ch.piece_hi; ++i) {
+            if (ch.pre(i)) continue;  // already up
             const int64_t off = i * pb, n = std::min(pb, hbytes - off);
             TSR_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d[1]) + off,
                                          static_cast<const char*>(host[parity]) + off, n,
@@ -548,6 +636,10 @@ Status run_host(const tsr_kernel* kk, const tsr_grid* gg, void* b0, void* b1, in
                                                                t_enq).count());
     if (chunked && same_halo)
         return run_chunked(*gg, g, t, o, c, host, parity, steps, ch, st, staged);
+    if (partial) {
+        cudaStreamSynchronize(c->stream);
+        return Status::Err(TSR_EUNSUPPORTED, "plane range with differing halos");
+    }
     if (staged) {  // differing halos: the whole read buffer after all
         TSR_CUDA_TRY(cudaMemcpyAsync(c->d[1], host[parity], hbytes, cudaMemcpyHostToDevice,
                                      c->stream));
@@ -627,15 +719,28 @@ Status run_host_single(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b
     return run_host(k, g, b0, b1, parity, steps, o, st);
 }
 
+bool range_chunkable(const Geo& g, const TapSet& t, int64_t steps, int64_t r_lo, int64_t r_hi) {
+    Chunks ch;
+    return plan_chunks(g, t, steps, r_lo, r_hi, &ch);
+}
+
+Status run_host_range(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b1, int parity,
+                      int64_t steps, const tsr_opts* o, tsr_stats* st, int64_t r_lo,
+                      int64_t r_hi, const std::function<void()>& after_margins, int cache_sub) {
+    return run_host(k, g, b0, b1, parity, steps, o, st, r_lo, r_hi, &after_margins, cache_sub);
+}
+
 // Frees what tsr_run caches per device (tsr_release_cache).
 void release_run_cache() {
     std::lock_guard<std::mutex> lock(g_cache_mu);
     int prev = 0;
     cudaGetDevice(&prev);
     for (size_t dev = 0; dev < g_cache.size(); ++dev) {
-        DeviceCache& c = g_cache[dev];
+        if (!g_cache[dev]) continue;
+        DeviceCache& c = *g_cache[dev];
+        std::lock_guard<std::mutex> held(c.mu);
         if (!c.stream && !c.stage && !c.d[0]) continue;
-        cudaSetDevice(static_cast<int>(dev));
+        cudaSetDevice(c.device);
         for (void*& p : c.d)
             if (p) {
                 cudaFree(p);

@@ -3,6 +3,7 @@
 // sweep dispatch and host<->device staging of BasicGrid<T> buffers.
 #pragma once
 
+#include <functional>
 #include <string>
 
 #include "common.cuh"
@@ -44,6 +45,16 @@ Status advance_grid(const Geo& g, const TapSet& t, const tsr_opts& o, void* d0, 
 Status run_host_single(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b1, int parity,
                        int64_t steps, const tsr_opts* o, tsr_stats* st);
 void release_run_cache();
+// The chunked round trip for the interior planes [r_lo, r_hi) of the
+// outermost axis only (one device's share of tsr_run_multi's short runs):
+// the planes its windows read beyond the range go up first, then
+// `after_margins` runs (the split round trip's barrier across devices),
+// then the pipeline.  TSR_EUNSUPPORTED when that path does not apply.
+bool range_chunkable(const Geo& g, const TapSet& t, int64_t steps, int64_t r_lo, int64_t r_hi);
+Status run_host_range(const tsr_kernel* k, const tsr_grid* g, void* b0, void* b1, int parity,
+                      int64_t steps, const tsr_opts* o, tsr_stats* st, int64_t r_lo,
+                      int64_t r_hi, const std::function<void()>& after_margins,
+                      int cache_sub = 0);
 
 // Sets the calling thread's device for a scope (and checks one exists).
 struct DeviceGuard {

@@ -394,3 +394,45 @@ def test_run_multi_differing_halos(ts, orc):
     assert st.fused_steps == 1 and g.parity == ref.parity
     for w in (0, 1):
         assert g.buffer(w).tobytes() == ref.buffer(w).tobytes(), w
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,extent,P", [("Heat-3D", [150, 20, 40], 2),
+                                           ("Heat-3D", [200, 18, 33], 3),
+                                           ("Box-2D9P", [300, 70], 2)])
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("per_slab", [False, True])
+def test_run_multi_split_round_trip(ts, orc, monkeypatch, name, extent, P, pinned, per_slab):
+    """Short runs of tsr_run_multi take the split round trip: every slab's
+    planes come from the chunked round trip on its device, the windows
+    reading the planes beyond the slab from the host buffers (no exchange),
+    after every range's margin planes are up (the barrier; per_slab runs one
+    range per slab, each with its own buffers, so the barrier spans several
+    ranges on one device).  Both buffers bitwise the oracle's and the slab
+    runtime's, odd and even T."""
+    k = _kernel(ts, name)
+    halo = [k.radius] * k.dims
+    monkeypatch.setenv("TSR_RUN_CHUNKED", "1")
+    if per_slab:
+        monkeypatch.setenv("TSR_SPLIT_PER_SLAB", "1")
+    for steps in (5, 4):
+        src = random_grid(ts, orc, extent, halo, 504)
+        g = src
+        if pinned:
+            g = ts.Grid(extent, halo, pinned=True)
+            for w in (0, 1):
+                g.buffer(w)[:] = src.buffer(w)
+        ref, slab = src.copy(), src.copy()
+        st = ts.run_multi(g, k, steps, P, devices=_devices(P))
+        orc.naive_run(ref, k, steps)
+        assert st.ngpus == P and st.messages == 0  # no exchange: replicated ghost zones
+        assert st.point_updates == int(np.prod(extent)) * steps
+        assert g.parity == ref.parity
+        for w in (0, 1):
+            assert g.buffer(w).tobytes() == ref.buffer(w).tobytes(), (name, steps, w)
+        monkeypatch.setenv("TSR_MULTI_SPLIT", "0")
+        st2 = ts.run_multi(slab, k, steps, P, devices=_devices(P))
+        monkeypatch.delenv("TSR_MULTI_SPLIT")
+        assert st2.messages > 0
+        for w in (0, 1):
+            assert slab.buffer(w).tobytes() == g.buffer(w).tobytes()
