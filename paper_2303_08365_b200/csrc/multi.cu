@@ -833,6 +833,7 @@ Status run_split(const tsr_kernel* kk, const tsr_grid* gg, const Geo& g, void* b
         out.h2d_bytes += sts[i].h2d_bytes;
         out.d2h_bytes += sts[i].d2h_bytes;
         out.device_ms = std::max(out.device_ms, sts[i].device_ms);
+        out.ghost_recompute_points += sts[i].ghost_recompute_points;
     }
     out.rounds = sts[0].rounds;
     out.trailing_steps = sts[0].trailing_steps;

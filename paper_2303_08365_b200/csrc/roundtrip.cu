@@ -414,6 +414,8 @@ Status run_chunked_impl(const tsr_grid& gg, const Geo& g, const TapSet& t, const
             local.engine = ws.engine;
         }
         local.kernel_launches += ws.kernel_launches;
+        // the window's planes beyond the chunk are swept and thrown away
+        local.ghost_recompute_points += ((wb - wa) - (b - a)) * (g.interior() / ch.n0) * steps;
         // planes [a, b) of steps T and T-1 into host layout
         Geo go = gw;
         go.n[ch.ax] = b - a;

@@ -426,6 +426,7 @@ def test_run_multi_split_round_trip(ts, orc, monkeypatch, name, extent, P, pinne
         st = ts.run_multi(g, k, steps, P, devices=_devices(P))
         orc.naive_run(ref, k, steps)
         assert st.ngpus == P and st.messages == 0  # no exchange: replicated ghost zones
+        assert st.ghost_recompute_points > 0  # the windows' margins, swept twice
         assert st.point_updates == int(np.prod(extent)) * steps
         assert g.parity == ref.parity
         for w in (0, 1):
